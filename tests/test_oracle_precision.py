@@ -1,0 +1,276 @@
+"""Pins for oracle/precision.py (O9).
+
+* rounding primitives: golden/rounding.json,
+  bitwise against the library casts of torch (a different implementation),
+  idempotence and unit-roundoff bounds;
+* the exact fp32 lowering of rational matrix entries (correct rounding);
+* special cases where fp arithmetic is exact (integer data, S:306 / S:315);
+* the paper's qualitative error claims (the absolute magnitudes are "parity
+  unpinned": Figure 1 is absent):
+    - error grows with tile size,
+    - at matched 2D ratio 2.25 the a^2+1 algorithm F(6x6) beats Toom-Cook F(4x4)
+      (SPEC acceptance 3),
+    - at 2D ratio 4 Toom-Cook F(2x2) beats F(3x3)+a^2+1 ("up to ratio around
+      3.5 for 2D"),
+    - 1D: at ratio 2.0 Toom-Cook wins, at ratio 1.5 the quadratic wins
+      ("up to ratio around 1.9 for 1D"),
+    - fp16 fails by range, bf16 does not (SPEC acceptance 6);
+* the pipeline model meets the north star's fp32 tolerance and its own a-priori
+  forward error bound.
+"""
+import json
+import os
+from fractions import Fraction as Fr
+
+import numpy as np
+import pytest
+import torch
+
+import datagen
+from oracle import conv as CV
+from oracle import metrics as MT
+from oracle import precision as P
+from oracle import transforms as T
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold():
+    with open(os.path.join(GOLD, "rounding.json")) as f:
+        return json.load(f)
+
+
+def _bits(a):
+    return np.asarray(a, np.float32).view(np.uint32)
+
+
+def test_golden_rounding():
+    g = _gold()
+    assert np.isinf(P.rd_fp16(np.float32(g["fp16_overflow"]["input"])))
+    assert P.rd_fp16(np.float32(g["fp16_max"]["input"])) == g["fp16_max"]["expect"]
+    x = np.array([int(g["bf16_trunc"]["input_bits"], 16)], np.uint32).view(np.float32)
+    assert _bits(P.rd_bf16(x, "trunc"))[0] == int(g["bf16_trunc"]["trunc_bits"], 16)
+    assert _bits(P.rd_bf16(x, "rne"))[0] == int(g["bf16_trunc"]["rne_bits"], 16)
+    u = np.array(g["fp16_dot_overflow"]["u"], np.float32)[None, :]
+    v = np.array(g["fp16_dot_overflow"]["v"], np.float32)
+    out = P.po_matmul(u, v, "fp16")
+    assert np.isinf(out[0])
+
+
+def _patterns(n, seed=0):
+    rng = np.random.default_rng(seed)
+    bits = rng.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    special = np.array([0, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00000, 1, 0x807FFFFF,
+                        0x3EAAAAAB, 0x477FE000, 0x477FF000, 0x477FEFFF, 0x7F7FFFFF, 0x33000000,
+                        0x33000001, 0x387FC000, 0x00FF8000], np.uint32)
+    return np.concatenate([special, bits]).view(np.float32)
+
+
+def test_bf16_rne_matches_library_cast():
+    a = _patterns(1 << 20)
+    ours = P.rd_bf16(a)
+    lib = torch.from_numpy(a.copy()).to(torch.bfloat16).to(torch.float32).numpy()
+    fin = ~np.isnan(a)
+    assert np.array_equal(_bits(ours)[fin], _bits(lib)[fin])
+    assert np.isnan(ours[~fin]).all()
+
+
+def test_fp16_matches_library_cast():
+    a = _patterns(1 << 20, 1)
+    ours = P.rd_fp16(a)
+    lib = torch.from_numpy(a.copy()).to(torch.float16).to(torch.float32).numpy()
+    fin = ~np.isnan(a)
+    assert np.array_equal(_bits(ours)[fin], _bits(lib)[fin])     # incl. subnormals and inf
+
+
+@pytest.mark.parametrize("dtype,mode,u", [("fp16", "rne", 2.0 ** -11), ("bf16", "rne", 2.0 ** -8),
+                                          ("bf16", "trunc", 2.0 ** -7)])
+def test_idempotence_and_bounds(dtype, mode, u):
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal(200000) * 10.0 ** rng.uniform(-3, 3, 200000)).astype(np.float32)
+    r = P.rd(dtype, x, mode)
+    assert np.array_equal(_bits(P.rd(dtype, r, mode)), _bits(r))
+    fin = np.isfinite(r) & (np.abs(x) > 1e-4)                                 # normal range
+    rel = np.abs(r[fin].astype(np.float64) - x[fin]) / np.abs(x[fin])
+    assert rel.max() <= u
+    x64 = rng.standard_normal(100000) * 1e3
+    assert (np.abs(P.rd_fp32(x64) - x64) <= 2.0 ** -24 * np.abs(x64)).all()
+
+
+def test_exact_fp32_lowering():
+    assert _bits(P.frac_to_f32(Fr(1, 3))) == 0x3EAAAAAB
+    assert P.frac_to_f32(Fr(-5, 4)) == np.float32(-1.25)
+    rng = np.random.default_rng(0)
+    for _ in range(2000):
+        fr = Fr(int(rng.integers(-10 ** 9, 10 ** 9)), int(rng.integers(1, 10 ** 9)))
+        f = P.frac_to_f32(fr)
+        lo = np.nextafter(f, np.float32(-np.inf))
+        hi = np.nextafter(f, np.float32(np.inf))
+        e = abs(Fr(float(f)) - fr)
+        assert e <= abs(Fr(float(lo)) - fr) and e <= abs(Fr(float(hi)) - fr)
+    # a halfway case between two fp32 values goes to even
+    a = np.float32(1.0)
+    half = (Fr(float(a)) + Fr(float(np.nextafter(a, np.float32(2))))) / 2
+    assert P.frac_to_f32(half) == a
+
+
+def test_integer_data_is_exact_in_fp32():
+    """S:306 / S:315: F(2,3) {0,1,-1,inf} with small integer data."""
+    ts = T.make_transforms("0,1,-1,inf", 2)
+    y = P.paper_conv1d(ts, np.array([[1, 2, 3, 4]]), np.array([[1, 1, 1]]), "fp32")
+    assert y.tolist() == [[6.0, 9.0]]
+    rng = np.random.default_rng(1)
+    x = rng.integers(-4, 5, (1, 3, 9, 9)).astype(np.float64)
+    w = rng.integers(-3, 4, (2, 3, 3, 3)).astype(np.float64)
+    for dtype in ("fp32", "fp16", "bf16"):
+        y = P.pipeline_conv2d(ts, x, w, dtype)
+        assert np.array_equal(y, CV.direct_conv2d_f64(x, w, 1)), dtype
+
+
+def test_zero_input_gives_zero():
+    ts = T.make_transforms(T.sup1(4), 4)
+    x = np.zeros((1, 2, 8, 8))
+    w = np.ones((2, 2, 3, 3))
+    for dtype in ("fp32", "fp16", "bf16"):
+        assert not P.pipeline_conv2d(ts, x, w, dtype).any()
+    assert not P.paper_conv1d(ts, np.zeros((4, 6)), np.ones((4, 3)), "fp16").any()
+
+
+# ------------------------------------------------------------------ qualitative claims (paper mode)
+
+
+def _tiles2d(S=5000, seed=0, nx=10):
+    rng = np.random.default_rng(seed)
+    g = datagen.draw(rng, (1, S, 3, 3), "paper_trunc_normal").astype(np.float32)
+    d = datagen.draw(rng, (1, S, nx, nx), "paper_trunc_normal").astype(np.float32)
+    return g.astype(np.float64), d.astype(np.float64)
+
+
+def _err2d(name, dtype, g, d):
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    dd = d[:, :, :m + 2, :m + 2]
+    Y = P.paper_conv2d_tiles(ts, dd, g, dtype)
+    ref = np.zeros((g.shape[1], m, m))
+    for p in range(3):
+        for q in range(3):
+            ref += g[0, :, p, q, None, None] * dd[0, :, p:p + m, q:q + m]
+    e = np.sqrt(((Y - ref) ** 2).sum(axis=(1, 2)))
+    return e / np.sqrt((ref ** 2).sum(axis=(1, 2)))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+def test_error_grows_with_tile_size_2d(dtype):
+    g, d = _tiles2d()
+    errs = [_err2d(f"lin{m}", dtype, g, d).mean() for m in range(2, 9)]
+    assert all(a < b for a, b in zip(errs, errs[1:])), errs
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+def test_ratio_matched_win_2d(dtype):
+    """SPEC acceptance 3: W F(6x6)+a^2+1 vs TC F(4x4), both ratio 2.25, 5000 paired trials."""
+    g, d = _tiles2d()
+    w6 = _err2d("sup1_6", dtype, g, d)
+    tc4 = _err2d("lin4", dtype, g, d)
+    assert w6.mean() < tc4.mean()
+    assert (w6 < tc4).mean() > 0.5
+
+
+def test_ratio4_toom_cook_wins_2d():
+    g, d = _tiles2d()
+    assert _err2d("lin2", "fp32", g, d).mean() < _err2d("sup1_3", "fp32", g, d).mean()
+
+
+def _err1d(mods, n, dtype, S=5000, seed=0):
+    ts = T.make_transforms(mods, n)
+    rng = np.random.default_rng(seed)
+    h = datagen.draw(rng, (S, 3), "paper_trunc_normal").astype(np.float32).astype(np.float64)
+    x = datagen.draw(rng, (S, n + 2), "paper_trunc_normal").astype(np.float32).astype(np.float64)
+    y = P.paper_conv1d(ts, x, h, dtype)
+    ref = np.stack([sum(h[:, k] * x[:, j + k] for k in range(3)) for j in range(n)], 1)
+    return MT.tile_rel_1d(y, ref)
+
+
+def test_1d_ratio_crossover():
+    # ratio 2.0: TC n=2 (mu 4) vs W n=3 (mu 6) -> TC wins
+    assert _err1d(T.lin(2), 2, "fp32").mean() < _err1d(T.sup1(3), 3, "fp32").mean()
+    # ratio 1.5: TC n=4 (mu 6) vs W n=6 (mu 9) -> W wins
+    assert _err1d(T.sup1(6), 6, "fp32").mean() < _err1d(T.lin(4), 4, "fp32").mean()
+
+
+def test_fp16_range_failure_bf16_not():
+    """SPEC acceptance 6 / P:596 (paper mode, per-op casts): inputs of magnitude
+    ~200 overflow fp16 intermediates but not bf16."""
+    ts = T.make_transforms(T.lin(8), 8)                    # Toom-Cook 8x8 (fp16 fails)
+    rng = np.random.default_rng(3)
+    d = 200.0 * rng.uniform(-1, 1, (2, 64, 10, 10))
+    g = rng.uniform(-2, 2, (2, 64, 3, 3))
+    y16 = P.paper_conv2d_tiles(ts, datagen.to_dtype_values(d, "fp16"), datagen.to_dtype_values(g, "fp16"), "fp16")
+    yb = P.paper_conv2d_tiles(ts, datagen.to_dtype_values(d, "bf16"), datagen.to_dtype_values(g, "bf16"), "bf16")
+    assert (~np.isfinite(y16)).sum() > 0
+    assert np.isfinite(yb).all()
+
+
+# ------------------------------------------------------------------ pipeline model vs tolerances
+
+
+@pytest.mark.parametrize("name", ["lin2", "lin4", "sup1_4", "sup1_6", "lin6", "lin8", "sup1_8"])
+def test_pipeline_fp32_meets_north_star_and_bound(name):
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    x, w = datagen.layer(1, 64, 16, 20, 20, "fp32", seed=m)
+    yref = CV.direct_conv2d_f64(x, w, 1)
+    y = P.pipeline_conv2d(ts, x, w, "fp32")
+    s = MT.summary(MT.stats8(y, yref, m))
+    assert s["rel_l1"] <= (1e-4 if m <= 4 else 1e-3)
+    S, gam, u_d = P.abs_bound_conv2d(ts, x, w, "fp32")
+    bound = 1.05 * ((2 * u_d + gam) * S + u_d * np.abs(yref))
+    assert (np.abs(y - yref) <= bound).all()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_pipeline_lowp_bound_and_ranking(dtype):
+    x, w = datagen.layer(1, 64, 16, 24, 24, dtype, seed=1)
+    yref = CV.direct_conv2d_f64(x, w, 1)
+    errs = {}
+    for name in ["lin4", "sup1_6"]:
+        mods, m = T.canonical(name)
+        ts = T.make_transforms(mods, m)
+        y = P.pipeline_conv2d(ts, x, w, dtype)
+        S, gam, u_d = P.abs_bound_conv2d(ts, x, w, dtype)
+        bound = 1.05 * ((2 * u_d + gam) * S + u_d * np.abs(yref))
+        assert (np.abs(y - yref) <= bound).all()
+        errs[name] = MT.summary(MT.stats8(y, yref, m))["mean_rel"]
+    assert errs["sup1_6"] < errs["lin4"]          # P:596 direction at ratio 2.25
+
+
+def test_residue_lowering_exact_with_integers():
+    for name in ["sup1_2", "sup1_4"]:           # dyadic matrices: exact in fp32
+        mods, m = T.canonical(name)
+        rb = T.residue_blocks(mods, m)
+        rng = np.random.default_rng(2)
+        x = rng.integers(-3, 4, (1, 2, 7, 7)).astype(np.float64)
+        w = rng.integers(-2, 3, (2, 2, 3, 3)).astype(np.float64)
+        y = P.pipeline_residue_conv2d(rb, x, w, "fp32")
+        assert np.array_equal(y, CV.direct_conv2d_f64(x, w, 1)), name
+
+
+def test_paper_mode_1d_fp32_is_plain_fp32():
+    """In fp32 the paper mode is plain fp32 evaluation without fused multiply-add."""
+    ts = T.make_transforms(T.lin(4), 4)
+    rng = np.random.default_rng(0)
+    x = rng.random((64, 6)).astype(np.float32)
+    h = rng.normal(0, 0.3, (64, 3)).astype(np.float32)
+    y = P.paper_conv1d(ts, x, h, "fp32")
+    G, BT, AT = P.lower_f32(ts.G), P.lower_f32(ts.BT), P.lower_f32(ts.AT)
+    for t in range(64):
+        def dot(row, v):
+            acc = np.float32(row[0] * v[0])
+            for j in range(1, len(v)):
+                acc = np.float32(acc + np.float32(row[j] * v[j]))
+            return acc
+        u = [dot(G[i], h[t]) for i in range(6)]
+        v = [dot(BT[i], x[t]) for i in range(6)]
+        p = [np.float32(a * b) for a, b in zip(u, v)]
+        yy = [dot(AT[i], p) for i in range(4)]
+        assert np.array_equal(np.array(yy, np.float32), y[t].astype(np.float32))
