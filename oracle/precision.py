@@ -318,14 +318,28 @@ def paper_conv2d_tiles(ts, d, g, dtype, bf16_mode="rne"):
 
 
 def abs_bound_conv2d(ts, x, w, dtype, pad=1, C_acc=None, mma_rel=0.0):
-    """Elementwise a-priori bound on |y_pipeline - y_exact| (first-order
-    running-error analysis of the pipeline model):
+    """First-order running-error analysis of the pipeline model (DESIGN.md
+    "Parity bounds"); see elementwise_bound for the complete bound.  Returns
+    (S, g, u_d):  S = |A|^T ( sum_c (|G||g||G|^T) (.) (|B|^T|d||B|) ) |A|,
+    g = (8 + 2 n_x + 2 + C + 2 mu + 2) u_32 + mma_rel."""
+    S, g, u_d, _ = _abs_bound_parts(ts, x, w, dtype, pad, C_acc, mma_rel)
+    return S, g, u_d
 
-        |dy| <= (2 u_d + g) * S + u_d * |y|,
-        S = |A|^T ( sum_c (|G||g||G|^T) (.) (|B|^T|d||B|) ) |A|,
-        g = (8 + 2 n_x + 2 + C + 2 mu + 2) u_32 + mma_rel,
 
-    computed in fp64 with exact |matrix| entries.  Returns (S, bound)."""
+# half the smallest subnormal: the absolute error of rounding an underflowing value
+ETA = {"fp32": 2.0 ** -150, "fp16": 2.0 ** -25, "bf16": 2.0 ** -134, "fp64": 0.0}
+
+
+def elementwise_bound(ts, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05):
+    """|y_pipeline - y_exact| <= (2 u_d + g) S + eta S_eta + u_d |y| + eta, with
+    S_eta = |A|^T ( sum_c (|G||g||G|^T) + (|B|^T|d||B|) + eta ) |A| the
+    propagation of underflow (absolute) errors of U and V (fp16 lin8 collapse)."""
+    S, g, u_d, S_eta = _abs_bound_parts(ts, x, w, dtype, pad, None, mma_rel)
+    eta = ETA[dtype]
+    return safety * ((2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta)
+
+
+def _abs_bound_parts(ts, x, w, dtype, pad, C_acc, mma_rel):
     u_d = UNIT_ROUNDOFF[dtype]
     u32 = UNIT_ROUNDOFF["fp32"]
     C = x.shape[1]
@@ -336,10 +350,13 @@ def abs_bound_conv2d(ts, x, w, dtype, pad=1, C_acc=None, mma_rel=0.0):
     m, mu = ts.n_o, ts.mu
     N, _, H, W = x.shape
     K = w.shape[0]
-    Ua = sep2(absG, np.abs(np.asarray(w, np.float64)).transpose(2, 3, 0, 1))
+    Ua = sep2(absG, np.abs(np.asarray(w, np.float64)).transpose(2, 3, 0, 1))          # (mu, mu, K, C)
     d, (Ho, Wo, th, tw) = halo_tiles(np.abs(np.asarray(x, np.float64)), m, ts.n_x, pad)
-    Va = sep2(absBT, d).transpose(0, 1, 2, 4, 5, 3).reshape(mu, mu, -1, C)
+    Va = sep2(absBT, d).transpose(0, 1, 2, 4, 5, 3).reshape(mu, mu, -1, C)            # (mu, mu, T, C)
     Ma = np.matmul(Ua, Va.transpose(0, 1, 3, 2))
     S = _scatter_tiles(sep2(absAT, Ma), N, K, th, tw, m, Ho, Wo)
+    eta = ETA[dtype]
+    Me = Ua.sum(axis=3)[:, :, :, None] + Va.sum(axis=3)[:, :, None, :] + eta * C        # (mu, mu, K, T)
+    S_eta = _scatter_tiles(sep2(absAT, Me), N, K, th, tw, m, Ho, Wo)
     g = (8 + 2 * ts.n_x + 2 + C_acc + 2 * mu + 2) * u32 + mma_rel
-    return S, g, u_d
+    return S, g, u_d, S_eta

@@ -1,0 +1,244 @@
+"""Thin Python binding over libwino.so (include/wino.h), same names as the C ABI.
+
+PyTorch provides device memory and the current CUDA stream only; every step of
+the path runs in the library's CUDA kernels.  Functions raise WinoError on any
+non-OK status; there is no CPU fallback.
+"""
+import ctypes
+from fractions import Fraction
+
+import numpy as np
+import torch
+
+from ._lib import DTYPES, LAYOUTS, LOWERINGS, WinoError, WinoModulus, check, lib
+
+_TORCH_DT = {torch.float32: "fp32", torch.float16: "fp16", torch.bfloat16: "bf16"}
+TORCH_OF = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _dt(t):
+    try:
+        return DTYPES[_TORCH_DT[t.dtype]]
+    except KeyError:
+        raise WinoError(1, f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def wino_parse_moduli(spec):
+    buf = (WinoModulus * 64)()
+    n = ctypes.c_int32()
+    check(lib().wino_parse_moduli(spec.encode(), buf, 64, ctypes.byref(n)))
+    return list(buf[:n.value])
+
+
+def _moduli_array(moduli):
+    if isinstance(moduli, str):
+        moduli = wino_parse_moduli(moduli)
+    arr = (WinoModulus * len(moduli))()
+    for i, m in enumerate(moduli):
+        arr[i] = m
+    return arr, len(moduli)
+
+
+class WinoAlgo:
+    """Owning handle of a generated algorithm (wino_make_transforms)."""
+
+    def __init__(self, moduli, m, r=3, sub_points=None, lowering="subsolver"):
+        self._h = None
+        mods, n = _moduli_array(moduli)
+        if sub_points is not None:
+            sub, ns = _moduli_array(sub_points)
+        else:
+            sub, ns = None, 0
+        h = ctypes.c_void_p()
+        check(lib().wino_make_transforms(mods, n, m, r, sub, ns, LOWERINGS[lowering], ctypes.byref(h)))
+        self._h = h
+        self.spec = moduli if isinstance(moduli, str) else None
+        self.lowering = lowering
+        vals = [ctypes.c_int32() for _ in range(5)]
+        ratio = ctypes.c_double()
+        check(lib().wino_algo_info(h, *[ctypes.byref(v) for v in vals], ctypes.byref(ratio)))
+        self.m, self.mu, self.nx, self.domain, self.units = (v.value for v in vals)
+        self.ratio_2d = ratio.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def matrix(self, which):
+        """(exact Fraction matrix, fp32 numpy matrix) of 'G', 'B' or 'A'."""
+        rows, cols = {"G": (self.domain, 3), "B": (self.nx, self.domain), "A": (self.domain, self.m)}[which]
+        num = np.zeros(rows * cols, np.int64)
+        den = np.zeros(rows * cols, np.int64)
+        f32 = np.zeros(rows * cols, np.float32)
+        check(lib().wino_algo_matrix(self._h, which.encode(), num.ctypes.data, den.ctypes.data, f32.ctypes.data))
+        exact = [[Fraction(int(num[i * cols + j]), int(den[i * cols + j])) for j in range(cols)] for i in range(rows)]
+        return exact, f32.reshape(rows, cols)
+
+    def unit_table(self):
+        u = self.units
+        out_pt, in_pt, nterm = (np.zeros(u, np.int32) for _ in range(3))
+        a = np.zeros((u, 4), np.int32)
+        coef = np.zeros((u, 4), np.float64)
+        check(lib().wino_algo_units(self._h, out_pt.ctypes.data, in_pt.ctypes.data, nterm.ctypes.data,
+                                    a.ctypes.data, coef.ctypes.data))
+        return out_pt, in_pt, nterm, a, coef
+
+    def close(self):
+        if self._h is not None:
+            lib().wino_algo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------- 2D layer
+
+
+def wino_conv2d_workspace(algo, N, C, H, W, K, pad=1, dtype="bf16", layout="nchw"):
+    b = ctypes.c_size_t()
+    check(lib().wino_conv2d_workspace(algo.handle, N, C, H, W, K, pad, DTYPES[dtype], LAYOUTS[layout],
+                                      ctypes.byref(b)))
+    return b.value
+
+
+def alloc_workspace(nbytes, device="cuda"):
+    """Device workspace, 1024-byte aligned (the TMA/UMMA swizzle atoms need it)."""
+    buf = torch.empty(nbytes + 1024, dtype=torch.uint8, device=device)
+    off = (-buf.data_ptr()) % 1024
+    return buf[off:off + nbytes]
+
+
+def wino_conv2d(x, w, algo, pad=1, layout="nchw", out=None, workspace=None, stream=None):
+    """y = conv(x, w) (valid cross-correlation, stride 1, zero padding `pad`)
+    through libwino's kernels.  x: [N,C,H,W], w: [K,C,3,3], same dtype, CUDA."""
+    assert layout == "nchw"
+    N, C, H, W = x.shape
+    K = w.shape[0]
+    assert w.shape == (K, C, 3, 3) and w.dtype == x.dtype and x.is_cuda and w.is_cuda
+    x = x.contiguous()
+    w = w.contiguous()
+    Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
+    if out is None:
+        out = torch.empty((N, K, Ho, Wo), dtype=x.dtype, device=x.device)
+    dt = _TORCH_DT[x.dtype]
+    nbytes = wino_conv2d_workspace(algo, N, C, H, W, K, pad, dt, layout)
+    if workspace is None:
+        workspace = alloc_workspace(nbytes, x.device)
+    check(lib().wino_conv2d(_ptr(x), _ptr(w), N, C, H, W, K, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
+                            _ptr(out), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return out
+
+
+def wino_conv2d_host_io(x_host, x_dev, w, algo, out_dev, out_host, workspace, pad=1, stream=None):
+    """End-to-end call: pinned host x -> device -> layer -> pinned host y, on `stream`."""
+    N, C, H, W = x_dev.shape
+    K = w.shape[0]
+    dt = _TORCH_DT[x_dev.dtype]
+    check(lib().wino_conv2d_host_io(_ptr(x_host), _ptr(x_dev), _ptr(w), N, C, H, W, K, pad, algo.handle,
+                                    DTYPES[dt], 0, _ptr(out_dev), _ptr(out_host), _ptr(workspace),
+                                    workspace.numel(), _stream(stream)))
+
+
+def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
+    """Workspace geometry (mirrors include/wino.h): sizes of U, V, M."""
+    m, D, S = algo.m, algo.domain, algo.units
+    Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
+    th, tw = -(-Ho // m), -(-Wo // m)
+    T = N * th * tw
+    return dict(Ho=Ho, Wo=Wo, th=th, tw=tw, T=T, Tp=-(-T // 4) * 4, Cp=-(-C // 64) * 64, Q=D * D, S=S,
+                planes=2 if dtype == "fp32" else 1)
+
+
+def wino_weight_transform(w, algo, stream=None):
+    """U [planes][S][K][Cp] in the storage dtype (fp32: hi, lo planes)."""
+    K, C = w.shape[:2]
+    dt = _TORCH_DT[w.dtype]
+    g = geometry(algo, 1, C, 3, 3, K, 1, dt)
+    U = torch.empty((g["planes"], g["S"], K, g["Cp"]), dtype=w.dtype, device=w.device)
+    check(lib().wino_weight_transform(_ptr(w.contiguous()), K, C, algo.handle, DTYPES[dt], _ptr(U), _stream(stream)))
+    return U
+
+
+def wino_input_transform(x, algo, pad=1, stream=None):
+    """V [planes][Q][T][Cp] in the storage dtype."""
+    N, C, H, W = x.shape
+    dt = _TORCH_DT[x.dtype]
+    g = geometry(algo, N, C, H, W, 1, pad, dt)
+    V = torch.empty((g["planes"], g["Q"], g["T"], g["Cp"]), dtype=x.dtype, device=x.device)
+    check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], 0, _ptr(V),
+                                     _stream(stream)))
+    return V
+
+
+def wino_domain_gemm(V, U, algo, C, K, stream=None):
+    """M [Q][K][Tp] fp32."""
+    T = V.shape[2]
+    dt = _TORCH_DT[V.dtype]
+    Tp = -(-T // 4) * 4
+    M = torch.empty((algo.domain ** 2, K, Tp), dtype=torch.float32, device=V.device)
+    check(lib().wino_domain_gemm(_ptr(V), _ptr(U), T, C, K, algo.handle, DTYPES[dt], _ptr(M), _stream(stream)))
+    return M
+
+
+def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None):
+    Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
+    y = torch.empty((N, K, Ho, Wo), dtype=TORCH_OF[dtype], device=M.device)
+    check(lib().wino_output_transform(_ptr(M), N, K, H, W, pad, algo.handle, DTYPES[dtype], 0, _ptr(y),
+                                      _stream(stream)))
+    return y
+
+
+# --------------------------------------------------------------------------- 1D tiles / metrics
+
+
+def wino_conv1d_tiles(x, h, algo, per_op_rounding=True, stream=None):
+    T = x.shape[0]
+    assert x.shape == (T, algo.m + 2) and h.shape == (T, 3) and x.dtype == h.dtype
+    y = torch.empty((T, algo.m), dtype=x.dtype, device=x.device)
+    check(lib().wino_conv1d_tiles(_ptr(x.contiguous()), _ptr(h.contiguous()), T, algo.handle, _dt(x),
+                                  1 if per_op_rounding else 0, _ptr(y), _stream(stream)))
+    return y
+
+
+def wino_error_stats(y, y_ref, m, stream=None):
+    """8 fp64 statistics (include/wino.h) of y vs the fp64 reference, on the device."""
+    N, K, Ho, Wo = y.shape
+    assert y_ref.shape == y.shape and y_ref.dtype == torch.float64
+    stats = torch.empty(8, dtype=torch.float64, device=y.device)
+    nbytes = lib().wino_error_stats_scratch(N, K, Ho, Wo, m)
+    scratch = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=y.device)
+    check(lib().wino_error_stats(_ptr(y.contiguous()), _dt(y), _ptr(y_ref.contiguous()), N, K, Ho, Wo, m,
+                                 _ptr(stats), _ptr(scratch), _stream(stream)))
+    return stats
+
+
+def wino_direct_conv2d_f64(x, w, pad=1, stream=None):
+    N, C, H, W = x.shape
+    K = w.shape[0]
+    y = torch.empty((N, K, H + 2 * pad - 2, W + 2 * pad - 2), dtype=torch.float64, device=x.device)
+    check(lib().wino_direct_conv2d_f64(_ptr(x.contiguous()), _ptr(w.contiguous()), N, C, H, W, K, pad, _dt(x),
+                                       _ptr(y), _stream(stream)))
+    return y
+
+
+def wino_last_launch_count():
+    return int(lib().wino_last_launch_count())
+
+
+def summary(stats):
+    s = stats.tolist() if hasattr(stats, "tolist") else list(stats)
+    return {"rel_l1": s[0] / s[1] if s[1] else float("nan"), "mean_rel": s[2] / s[6],
+            "mean_euclid": s[3] / s[6], "max_rel": s[4], "nonfinite": int(s[5]), "tiles": int(s[6])}

@@ -1,0 +1,81 @@
+"""Build libwino.so in-tree: nvcc for sm_100a (tcgen05 / TMA need the 'a'
+target), -lineinfo for ncu source mapping, no --use_fast_math (subnormals and
+round-to-nearest-even must be kept, readings A10/A11).
+
+    python -m paper_1905_05233_b200.build [--force] [-j N]
+"""
+import argparse
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build_obj")
+LIB = os.path.join(HERE, "libwino.so")
+SOURCES = ["capi_host.cpp", "generator.cpp", "transforms.cu", "xform_f32.cu", "xform_f16.cu", "xform_bf16.cu",
+           "gemm.cu", "conv.cu", "misc.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _flags(src):
+    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall"]
+    if src.endswith(".cu"):
+        return ARCH + common + ["-lineinfo", "-Xptxas", "-warn-spills"]
+    return ["-x", "c++"] + common
+
+
+def _deps():
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "wino.h")]
+
+
+def build(force=False, jobs=None, verbose=False):
+    os.makedirs(OBJ, exist_ok=True)
+    dep_mtime = max(os.path.getmtime(p) for p in _deps())
+    objs, todo = [], []
+    for s in SOURCES:
+        o = os.path.join(OBJ, s + ".o")
+        objs.append(o)
+        if force or not os.path.exists(o) or os.path.getmtime(o) < dep_mtime:
+            todo.append((s, o))
+
+    def compile_one(item):
+        s, o = item
+        cmd = [nvcc()] + _flags(s) + ["-c", os.path.join(CSRC, s), "-o", o]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        if verbose and (r.stdout or r.stderr):
+            print(r.stdout + r.stderr)
+        return s
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 1)) as ex:
+            for s in ex.map(compile_one, todo):
+                if verbose:
+                    print("compiled", s)
+    if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs + ["-lcuda"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-j", type=int, default=None)
+    a = ap.parse_args()
+    print(build(a.force, a.j, verbose=True))
+    sys.exit(0)

@@ -1,0 +1,123 @@
+// conv.cu -- C-ABI device entry points of the 2D layer (include/wino.h):
+// wino_conv2d = K2 weight transform -> K1 input transform -> K3 tcgen05
+// Winograd-domain GEMM -> K4 output transform, all on the caller's stream.
+#include <string>
+
+#include "device.cuh"
+#include "geometry.hpp"
+
+namespace wino {
+wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* al, wino_dtype dt, void* U,
+                                 cudaStream_t st);
+wino_status run_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
+                                wino_dtype dt, wino_layout layout, void* V, cudaStream_t st);
+wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
+                            float* M, cudaStream_t st);
+wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
+                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st);
+}  // namespace wino
+
+using namespace wino;
+
+static wino_status check_layer(const wino_algo* al, int N, int C, int H, int W, int K, int pad, wino_dtype dt,
+                               wino_layout layout) {
+  if (!al) return set_last_error("NULL algo"), WINO_E_ARG;
+  if (N <= 0 || C <= 0 || K <= 0 || (pad != 0 && pad != 1) || H + 2 * pad < 3 || W + 2 * pad < 3)
+    return set_last_error("bad layer geometry (need N, C, K > 0, pad in {0,1}, H, W + 2 pad >= 3)"), WINO_E_ARG;
+  if (dt != WINO_F32 && dt != WINO_F16 && dt != WINO_BF16) return set_last_error("bad dtype"), WINO_E_ARG;
+  if (layout != WINO_NCHW && layout != WINO_NHWC) return set_last_error("bad layout"), WINO_E_ARG;
+  if (layout != WINO_NCHW) return set_last_error("NHWC layout not implemented yet"), WINO_E_UNSUPPORTED;
+  if (al->r != 3) return set_last_error("r != 3"), WINO_E_UNSUPPORTED;
+  if (K > 65535) return set_last_error("K > 65535 unsupported"), WINO_E_UNSUPPORTED;
+  return WINO_OK;
+}
+
+extern "C" {
+
+wino_status wino_conv2d_workspace(const wino_algo* al, int N, int C, int H, int W, int K, int pad,
+                                  wino_dtype dt, wino_layout layout, size_t* bytes) {
+  if (!bytes) return set_last_error("NULL bytes"), WINO_E_ARG;
+  wino_status s = check_layer(al, N, C, H, W, K, pad, dt, layout);
+  if (s != WINO_OK) return s;
+  *bytes = make_geo(al, N, C, H, W, K, pad, dt).total;
+  return WINO_OK;
+}
+
+wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W, int K, int pad,
+                        const wino_algo* al, wino_dtype dt, wino_layout layout, void* out, void* ws,
+                        size_t ws_bytes, void* stream) {
+  reset_launch_count();
+  wino_status s = check_layer(al, N, C, H, W, K, pad, dt, layout);
+  if (s != WINO_OK) return s;
+  if (!x || !w || !out || !ws) return set_last_error("NULL buffer"), WINO_E_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) % 1024) return set_last_error("workspace must be 1024-byte aligned"), WINO_E_ARG;
+  Geo g = make_geo(al, N, C, H, W, K, pad, dt);
+  if (ws_bytes < g.total) return set_last_error("workspace too small"), WINO_E_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* base = static_cast<char*>(ws);
+  void* U = base + g.offU;
+  void* V = base + g.offV;
+  float* M = reinterpret_cast<float*>(base + g.offM);
+  if ((s = run_weight_transform(w, K, C, al, dt, U, st)) != WINO_OK) return s;
+  if ((s = run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, st)) != WINO_OK) return s;
+  if ((s = run_domain_gemm(V, U, g, al, dt, M, st)) != WINO_OK) return s;
+  if ((s = run_output_transform(M, N, K, H, W, pad, al, dt, layout, out, st)) != WINO_OK) return s;
+  return WINO_OK;
+}
+
+wino_status wino_conv2d_host_io(const void* x_host, void* x_dev, const void* w_dev, int N, int C, int H, int W,
+                                int K, int pad, const wino_algo* al, wino_dtype dt, wino_layout layout,
+                                void* out_dev, void* out_host, void* ws, size_t ws_bytes, void* stream) {
+  wino_status s = check_layer(al, N, C, H, W, K, pad, dt, layout);
+  if (s != WINO_OK) return s;
+  if (!x_host || !out_host || !x_dev || !out_dev) return set_last_error("NULL buffer"), WINO_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Geo g = make_geo(al, N, C, H, W, K, pad, dt);
+  size_t xb = (size_t)N * C * H * W * g.es, yb = (size_t)N * K * g.Ho * g.Wo * g.es;
+  WINO_CUDA_CHECK(cudaMemcpyAsync(x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
+  s = wino_conv2d(x_dev, w_dev, N, C, H, W, K, pad, al, dt, layout, out_dev, ws, ws_bytes, stream);
+  if (s != WINO_OK) return s;
+  WINO_CUDA_CHECK(cudaMemcpyAsync(out_host, out_dev, yb, cudaMemcpyDeviceToHost, st));
+  return WINO_OK;
+}
+
+wino_status wino_weight_transform(const void* w, int K, int C, const wino_algo* al, wino_dtype dt, void* U,
+                                  void* stream) {
+  reset_launch_count();
+  wino_status s = check_layer(al, 1, C, 3, 3, K, 0, dt, WINO_NCHW);
+  if (s != WINO_OK) return s;
+  if (!w || !U) return set_last_error("NULL buffer"), WINO_E_ARG;
+  return run_weight_transform(w, K, C, al, dt, U, reinterpret_cast<cudaStream_t>(stream));
+}
+
+wino_status wino_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
+                                 wino_dtype dt, wino_layout layout, void* V, void* stream) {
+  reset_launch_count();
+  wino_status s = check_layer(al, N, C, H, W, 1, pad, dt, layout);
+  if (s != WINO_OK) return s;
+  if (!x || !V) return set_last_error("NULL buffer"), WINO_E_ARG;
+  return run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, reinterpret_cast<cudaStream_t>(stream));
+}
+
+wino_status wino_domain_gemm(const void* V, const void* U, int T, int C, int K, const wino_algo* al,
+                             wino_dtype dt, float* M, void* stream) {
+  reset_launch_count();
+  if (!al || !V || !U || !M || T <= 0 || C <= 0 || K <= 0) return set_last_error("bad argument"), WINO_E_ARG;
+  if (reinterpret_cast<uintptr_t>(V) % 16 || reinterpret_cast<uintptr_t>(U) % 16)
+    return set_last_error("V and U must be 16-byte aligned"), WINO_E_ARG;
+  Geo g = make_geo(al, 1, C, 3, 3, K, 0, dt);  // Cp, Q, S, es, planes
+  g.T = T;
+  g.Tp = (int)align_up(T, 4);
+  return run_domain_gemm(V, U, g, al, dt, M, reinterpret_cast<cudaStream_t>(stream));
+}
+
+wino_status wino_output_transform(const float* M, int N, int K, int H, int W, int pad, const wino_algo* al,
+                                  wino_dtype dt, wino_layout layout, void* out, void* stream) {
+  reset_launch_count();
+  wino_status s = check_layer(al, N, 1, H, W, K, pad, dt, layout);
+  if (s != WINO_OK) return s;
+  if (!M || !out) return set_last_error("NULL buffer"), WINO_E_ARG;
+  return run_output_transform(M, N, K, H, W, pad, al, dt, layout, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+// gemm.cu -- K3: the Winograd-domain channel reduction on the 5th-generation
+// tensor cores (the Hadamard product, summed over input
+// channels, "dominates the execution time" of DNN Winograd convolution):
+//
+//     M_p[k][t] = sum_{(q, u) in sched(p)} sum_c U_u[k][c] * V_q[t][c]
+//
+// SUBSOLVER lowering: sched(p) = {(p, p)} -- mu^2 independent GEMMs.
+// RESIDUE lowering:   sched(p) = the block-pair units of output point p (the
+// "2x2-block polynomial product mod m_i" contracting C x |I| x |J|).
+//
+// Design (sm_100a): persistent, warp-specialised, one CTA per SM.
+//   warp 0      TMA producer: A = V_q tile [128 t x BK c], B = U_u tile
+//               [BN k x BK c], both K-major with the 128-byte swizzle, into a
+//               STAGES-deep mbarrier ring.
+//   warp 1      MMA issuer (one thread): tcgen05.mma.cta_group::1, M = 128,
+//               N = BN, fp32 accumulators in TMEM (2 x BN columns, double
+//               buffered so the epilogue of item i overlaps the MMAs of i+1).
+//               kind::f16 for fp16/bf16; fp32 runs three kind::tf32 products
+//               hi*hi + hi*lo + lo*hi per K step (hi/lo planes made by K1/K2).
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (TMEM lane = tile t) and
+//               coalesced stores of M[p][k][t] (a warp writes 128 contiguous
+//               bytes per k).
+#include <string>
+
+#include "device.cuh"
+#include "geometry.hpp"
+
+namespace wino {
+
+constexpr int kBM = 128;
+
+template <bool kTF32, int BN, int STAGES>
+struct GemmCfg {
+  static constexpr int ES = kTF32 ? 4 : 2;
+  static constexpr int BK = 128 / ES;   // elements per 128-byte swizzled row
+  static constexpr int UK = kTF32 ? 8 : 16;
+  static constexpr int NPL = kTF32 ? 2 : 1;
+  static constexpr int A_BYTES = kBM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <bool kTF32, int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    domain_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                       float* __restrict__ Mout, int T, int K, int Tp, int Cp, int nMB, int nNB, int Q, int S,
+                       uint32_t idesc, const __grid_constant__ GemmSched gs) {
+  using Cfg = GemmCfg<kTF32, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmU);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
+    fence_barrier_init();
+    fence_proxy_async_shared();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nItems = Q * nMB * nNB;
+  const int KB = Cp / Cfg::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+        const int nb = item % nNB, mb = (item / nNB) % nMB, p = item / (nNB * nMB);
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          const int qi = gs.in_pt[pr], sl = gs.slab[pr];
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
+            tma_load_3d(base, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi);
+            if constexpr (kTF32) tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi + Q);
+            uint8_t* bb = base + Cfg::NPL * Cfg::A_BYTES;
+            tma_load_3d(bb, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
+            if constexpr (kTF32) tma_load_3d(bb + Cfg::B_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl + S);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+        const int p = item / (nNB * nMB);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        int step = 0;
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          for (int kb = 0; kb < KB; ++kb, ++step) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t b0 = a0 + Cfg::NPL * Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint32_t koff = k * Cfg::UK * Cfg::ES;  // 32 bytes
+              mma_ss<kTF32>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc,
+                            (step | k) != 0);
+              if constexpr (kTF32) {
+                mma_ss<true>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + Cfg::B_BYTES + koff), idesc, 1);
+                mma_ss<true>(d_tmem, umma_desc_sw128(a0 + Cfg::A_BYTES + koff), umma_desc_sw128(b0 + koff), idesc, 1);
+              }
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) acc = 0, acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue
+    const int wq = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+      const int nb = item % nNB, mb = (item / nNB) % nMB, p = item / (nNB * nMB);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int t = mb * kBM + wq * 32 + lane;
+      float* out = Mout + ((size_t)p * K + (size_t)nb * BN) * Tp + t;
+      const int kmax = min(BN, K - nb * BN);
+#pragma unroll 1
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
+        if (t < T) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj)
+            if (j0 + jj < kmax) out[(size_t)(j0 + jj) * Tp] = v[jj];
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) acc = 0, acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+static bool make_map3(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, uint64_t d0,
+                      uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * es, d0 * d1 * es};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <bool kTF32, int BN, int STAGES>
+static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, float* M, const Geo& g,
+                               const GemmSched& gs, uint32_t fmt, cudaStream_t st) {
+  using Cfg = GemmCfg<kTF32, BN, STAGES>;
+  auto kern = domain_gemm_kernel<kTF32, BN, STAGES>;
+  static bool attr = false;
+  if (!attr) {
+    WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr = true;
+  }
+  const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
+  const int items = g.Q * nMB * nNB;
+  const int grid = items < num_sms() ? items : num_sms();
+  kern<<<grid, 256, Cfg::SMEM, st>>>(tv, tu, M, g.T, g.K, g.Tp, g.Cp, nMB, nNB, g.Q, g.S,
+                                     make_idesc(fmt, kBM, BN), gs);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
+                            float* M, cudaStream_t st) {
+  const bool tf32 = dt == WINO_F32;
+  CUtensorMapDataType cdt = dt == WINO_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                            : dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  int BN = tf32 ? (g.K > 64 ? 128 : 64) : (g.K > 128 ? 256 : (g.K > 64 ? 128 : 64));
+  const uint32_t BK = 128 / (uint32_t)g.es;
+  CUtensorMap tv, tu;
+  if (!make_map3(&tv, cdt, g.es, V, g.Cp, g.T, (uint64_t)g.Q * g.planes, BK, kBM) ||
+      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN)) {
+    set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
+    return WINO_E_CUDA;
+  }
+  // UMMA operand formats: kind::f16 F16 = 0, BF16 = 1; kind::tf32 TF32 = 2.
+  const uint32_t fmt = dt == WINO_F16 ? 0u : dt == WINO_BF16 ? 1u : 2u;
+  if (tf32) {
+    if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, M, g, al->gs, fmt, st);
+    return launch_gemm<true, 64, 4>(tv, tu, M, g, al->gs, fmt, st);
+  }
+  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, M, g, al->gs, fmt, st);
+  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, M, g, al->gs, fmt, st);
+  return launch_gemm<false, 64, 8>(tv, tu, M, g, al->gs, fmt, st);
+}
+
+}  // namespace wino

@@ -1,0 +1,47 @@
+// geometry.hpp -- layer geometry and workspace layout of wino_conv2d
+// (include/wino.h): U [S][K][Cp] | V [Q][T][Cp] | M [Q][K][Tp] fp32.
+#pragma once
+#include <cstddef>
+
+#include "algo.hpp"
+
+namespace wino {
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Geo {
+  int N, C, H, W, K, pad;
+  int m, D, Q, S;
+  int Ho, Wo, th, tw, T, Tp, Cp;
+  size_t es, planes;
+  size_t offU, offV, offM, total;
+};
+
+// Tiling of PAPER.md P:498: overlapping (m+2)x(m+2) tiles at stride m.
+inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int pad, wino_dtype dt) {
+  Geo g;
+  g.N = N, g.C = C, g.H = H, g.W = W, g.K = K, g.pad = pad;
+  g.m = al->m;
+  g.D = al->D;
+  g.Q = al->D * al->D;
+  g.S = al->units;
+  g.Ho = H + 2 * pad - 2;
+  g.Wo = W + 2 * pad - 2;
+  g.th = (g.Ho + g.m - 1) / g.m;
+  g.tw = (g.Wo + g.m - 1) / g.m;
+  g.T = N * g.th * g.tw;
+  g.Tp = (int)align_up(g.T, 4);
+  g.Cp = (int)align_up(C, 64);
+  g.es = dt == WINO_F32 ? 4 : 2;
+  g.planes = dt == WINO_F32 ? 2 : 1;  // fp32: TF32 hi and lo planes
+  size_t u_bytes = g.planes * (size_t)g.S * K * g.Cp * g.es;
+  size_t v_bytes = g.planes * (size_t)g.Q * g.T * g.Cp * g.es;
+  size_t m_bytes = (size_t)g.Q * K * g.Tp * 4;
+  g.offU = 0;
+  g.offV = align_up(g.offU + u_bytes, 1024);
+  g.offM = align_up(g.offV + v_bytes, 1024);
+  g.total = align_up(g.offM + m_bytes, 1024);
+  return g;
+}
+
+}  // namespace wino

@@ -1,0 +1,295 @@
+// misc.cu -- K5 batched 1D tiles (BASELINE cfg 2), K6 error statistics, the
+// fp64 direct-convolution reference of the metric path, launch accounting.
+#include <string>
+
+#include "device.cuh"
+#include "geometry.hpp"
+
+namespace wino {
+
+static thread_local int g_launches = 0;
+void count_launch(int n) { g_launches += n; }
+void reset_launch_count() { g_launches = 0; }
+
+// ------------------------------------------------------------------ K5: 1D tiles
+// y = A^T [(G h) (.) (B^T x)] per tile.  PAPER=true: every
+// scalar multiply/add in fp32 without contraction (__fmul_rn / __fadd_rn), cast
+// to the dtype after each op, ascending index from the first product, matrix
+// entries cast once.  PAPER=false: fp32 internally, u, v, y rounded.
+template <int DT, int M, int MU, bool PAPER>
+__global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<DT>::T* __restrict__ x,
+                                                           const typename DType<DT>::T* __restrict__ h, int64_t T,
+                                                           const __grid_constant__ XformParams xp,
+                                                           typename DType<DT>::T* __restrict__ y) {
+  using Tr = DType<DT>;
+  constexpr int NX = M + 2;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float hv[3], xv[NX];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) hv[j] = Tr::load(h + t * 3 + j);
+#pragma unroll
+  for (int j = 0; j < NX; ++j) xv[j] = Tr::load(x + t * NX + j);
+  float p[MU];
+#pragma unroll
+  for (int i = 0; i < MU; ++i) {
+    float u, v;
+    if constexpr (PAPER) {
+      u = Tr::rd(__fmul_rn(Tr::rd(xp.G[i][0]), hv[0]));
+#pragma unroll
+      for (int j = 1; j < 3; ++j) u = Tr::rd(__fadd_rn(u, Tr::rd(__fmul_rn(Tr::rd(xp.G[i][j]), hv[j]))));
+      v = Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][0]), xv[0]));
+#pragma unroll
+      for (int j = 1; j < NX; ++j) v = Tr::rd(__fadd_rn(v, Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][j]), xv[j]))));
+      p[i] = Tr::rd(__fmul_rn(u, v));
+    } else {
+      u = 0.f, v = 0.f;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) u = fmaf(xp.G[i][j], hv[j], u);
+#pragma unroll
+      for (int j = 0; j < NX; ++j) v = fmaf(xp.BT[i][j], xv[j], v);
+      p[i] = __fmul_rn(Tr::rd(u), Tr::rd(v));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q) {
+    float acc;
+    if constexpr (PAPER) {
+      acc = Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][0]), p[0]));
+#pragma unroll
+      for (int i = 1; i < MU; ++i) acc = Tr::rd(__fadd_rn(acc, Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][i]), p[i]))));
+    } else {
+      acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < MU; ++i) acc = fmaf(xp.AT[q][i], p[i], acc);
+    }
+    y[t * M + q] = Tr::cvt(acc);
+  }
+}
+
+struct C1Args {
+  const void *x, *h;
+  int64_t T;
+  const XformParams* xp;
+  void* y;
+  cudaStream_t st;
+};
+template <int DT, int M, int MU, bool P>
+static void launch_c1(const C1Args& a) {
+  using Tr = DType<DT>;
+  conv1d_tiles_kernel<DT, M, MU, P><<<(unsigned)((a.T + 127) / 128), 128, 0, a.st>>>(
+      (const typename Tr::T*)a.x, (const typename Tr::T*)a.h, a.T, *a.xp, (typename Tr::T*)a.y);
+}
+using C1Fn = void (*)(const C1Args&);
+#define C1ROW(DT, M, P) {&launch_c1<DT, M, M + 2, P>, &launch_c1<DT, M, M + 3, P>, &launch_c1<DT, M, M + 4, P>}
+#define C1TAB(DT, P) {C1ROW(DT, 2, P), C1ROW(DT, 3, P), C1ROW(DT, 4, P), C1ROW(DT, 5, P), C1ROW(DT, 6, P), C1ROW(DT, 7, P), C1ROW(DT, 8, P)}
+static const C1Fn kC1[2][3][7][3] = {
+    {C1TAB(WINO_F32, false), C1TAB(WINO_F16, false), C1TAB(WINO_BF16, false)},
+    {C1TAB(WINO_F32, true), C1TAB(WINO_F16, true), C1TAB(WINO_BF16, true)}};
+
+// ------------------------------------------------------------------ K6: error statistics
+constexpr int kStatThreads = 256;
+
+__device__ __forceinline__ void stat_combine(double* a, const double* b) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (i == 4) ? fmax(a[i], b[i]) : a[i] + b[i];
+}
+
+// fixed-order tree reduction of 8 doubles per thread over the block
+__device__ void block_reduce8(double* v, double (*sh)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sh[threadIdx.x][i] = v[i];
+  __syncthreads();
+  for (int s = kStatThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) stat_combine(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kStatThreads) stats_tiles_kernel(const typename DType<DT>::T* __restrict__ y,
+                                                                   const double* __restrict__ yr, int N, int K,
+                                                                   int Ho, int Wo, int m, int th, int tw,
+                                                                   double* __restrict__ part) {
+  using Tr = DType<DT>;
+  __shared__ double sh[kStatThreads][8];
+  const int64_t ntiles = (int64_t)N * K * th * tw;
+  const int64_t tile = (int64_t)blockIdx.x * kStatThreads + threadIdx.x;
+  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (tile < ntiles) {
+    const int tj = (int)(tile % tw);
+    int64_t r = tile / tw;
+    const int ti = (int)(r % th);
+    const int64_t nk = r / th;
+    double sad = 0, sar = 0, e2 = 0, r2 = 0, nf = 0, ne = 0;
+    for (int p = 0; p < m; ++p) {
+      const int i = ti * m + p;
+      if (i >= Ho) break;
+      for (int q = 0; q < m; ++q) {
+        const int j = tj * m + q;
+        if (j >= Wo) break;
+        const size_t off = ((size_t)nk * Ho + i) * Wo + j;
+        const double yy = (double)Tr::load(y + off), rr = yr[off];
+        double d;
+        if (isfinite(yy)) {
+          d = fabs(yy - rr);
+        } else {
+          d = INFINITY;
+          nf += 1;
+        }
+        sad += d;
+        sar += fabs(rr);
+        e2 += d * d;
+        r2 += rr * rr;
+        ne += 1;
+      }
+    }
+    const double e = sqrt(e2), rn = sqrt(r2);
+    const double rel = e == 0 ? 0.0 : (rn == 0 ? INFINITY : e / rn);
+    v[0] = sad, v[1] = sar, v[2] = rel, v[3] = e, v[4] = rel, v[5] = nf, v[6] = 1, v[7] = ne;
+  }
+  block_reduce8(v, sh);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 8; ++i) part[(size_t)blockIdx.x * 8 + i] = sh[0][i];
+}
+
+__global__ void __launch_bounds__(kStatThreads) stats_final_kernel(const double* __restrict__ part, int nparts,
+                                                                   double* __restrict__ out) {
+  __shared__ double sh[kStatThreads][8];
+  double v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nparts; b += kStatThreads) stat_combine(v, part + (size_t)b * 8);
+  block_reduce8(v, sh);
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 8; ++i) out[i] = sh[0][i];
+}
+
+// ------------------------------------------------------------------ fp64 direct reference
+// y_ref[n,k,i,j] = sum_{c,p,q} w[k,c,p,q] x[n,c,i+p-pad,j+q-pad]  (valid
+// cross-correlation, zero padding).  CTA = 32 output columns x
+// 32 output channels of one (n, i) row; x rows and weights staged per channel.
+template <int DT>
+__global__ void __launch_bounds__(256) direct_f64_kernel(const typename DType<DT>::T* __restrict__ x,
+                                                         const typename DType<DT>::T* __restrict__ w, int C, int H,
+                                                         int W, int K, int pad, int Ho, int Wo,
+                                                         double* __restrict__ y) {
+  using Tr = DType<DT>;
+  __shared__ double xs[3][34];
+  __shared__ double wsm[32][9];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 groups of 4 channels
+  const int j0 = blockIdx.x * 32;
+  const int n = blockIdx.y / Ho, i = blockIdx.y % Ho;
+  const int k0 = blockIdx.z * 32;
+  double acc[4] = {0, 0, 0, 0};
+  for (int c = 0; c < C; ++c) {
+    for (int e = threadIdx.x; e < 3 * 34; e += 256) {
+      const int p = e / 34, q = e % 34;
+      const int r = i + p - pad, col = j0 + q - pad;
+      xs[p][q] = (r >= 0 && r < H && col >= 0 && col < W) ? (double)Tr::load(x + (((size_t)n * C + c) * H + r) * W + col) : 0.0;
+    }
+    for (int e = threadIdx.x; e < 32 * 9; e += 256) {
+      const int kk = e / 9, pq = e % 9;
+      wsm[kk][pq] = (k0 + kk < K) ? (double)Tr::load(w + ((size_t)(k0 + kk) * C + c) * 9 + pq) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+      for (int p = 0; p < 3; ++p)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[kk] = fma(wsm[ty * 4 + kk][p * 3 + q], xs[p][tx + q], acc[kk]);
+    __syncthreads();
+  }
+  const int j = j0 + tx;
+  if (j < Wo)
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = k0 + ty * 4 + kk;
+      if (k < K) y[(((size_t)n * K + k) * Ho + i) * Wo + j] = acc[kk];
+    }
+}
+
+}  // namespace wino
+
+using namespace wino;
+
+extern "C" {
+
+int32_t wino_last_launch_count(void) { return g_launches; }
+
+wino_status wino_conv1d_tiles(const void* x, const void* h, int64_t T, const wino_algo* al, wino_dtype dt,
+                              int per_op_rounding, void* y, void* stream) {
+  reset_launch_count();
+  if (!al || !x || !h || !y || T < 0) return set_last_error("bad argument"), WINO_E_ARG;
+  if (dt != WINO_F32 && dt != WINO_F16 && dt != WINO_BF16) return set_last_error("bad dtype"), WINO_E_ARG;
+  if (al->lowering != WINO_LOWER_SUBSOLVER) return set_last_error("1D tiles: SUBSOLVER algos only"), WINO_E_UNSUPPORTED;
+  const int dm = al->mu - al->m - 2;
+  if (dm < 0 || dm > 2) return set_last_error("1D tiles: mu must be in [m+2, m+4]"), WINO_E_UNSUPPORTED;
+  if (T == 0) return WINO_OK;
+  C1Args a{x, h, T, &al->xp, y, reinterpret_cast<cudaStream_t>(stream)};
+  kC1[per_op_rounding ? 1 : 0][dt][al->m - 2][dm](a);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+size_t wino_error_stats_scratch(int N, int K, int Ho, int Wo, int m) {
+  if (N <= 0 || K <= 0 || Ho <= 0 || Wo <= 0 || m <= 0) return 0;
+  int64_t tiles = (int64_t)N * K * ((Ho + m - 1) / m) * ((Wo + m - 1) / m);
+  return (size_t)((tiles + kStatThreads - 1) / kStatThreads) * 8 * sizeof(double);
+}
+
+wino_status wino_error_stats(const void* y, wino_dtype dt, const double* y_ref, int N, int K, int Ho, int Wo, int m,
+                             double* stats, void* scratch, void* stream) {
+  reset_launch_count();
+  if (!y || !y_ref || !stats || !scratch || N <= 0 || K <= 0 || Ho <= 0 || Wo <= 0 || m <= 0)
+    return set_last_error("bad argument"), WINO_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int th = (Ho + m - 1) / m, tw = (Wo + m - 1) / m;
+  const int64_t tiles = (int64_t)N * K * th * tw;
+  const int nb = (int)((tiles + kStatThreads - 1) / kStatThreads);
+  double* part = static_cast<double*>(scratch);
+  switch (dt) {
+    case WINO_F32:
+      stats_tiles_kernel<WINO_F32><<<nb, kStatThreads, 0, st>>>((const float*)y, y_ref, N, K, Ho, Wo, m, th, tw, part);
+      break;
+    case WINO_F16:
+      stats_tiles_kernel<WINO_F16><<<nb, kStatThreads, 0, st>>>((const __half*)y, y_ref, N, K, Ho, Wo, m, th, tw, part);
+      break;
+    case WINO_BF16:
+      stats_tiles_kernel<WINO_BF16><<<nb, kStatThreads, 0, st>>>((const __nv_bfloat16*)y, y_ref, N, K, Ho, Wo, m,
+                                                                 th, tw, part);
+      break;
+    default:
+      return set_last_error("bad dtype"), WINO_E_ARG;
+  }
+  WINO_LAUNCH_CHECK();
+  stats_final_kernel<<<1, kStatThreads, 0, st>>>(part, nb, stats);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+wino_status wino_direct_conv2d_f64(const void* x, const void* w, int N, int C, int H, int W, int K, int pad,
+                                   wino_dtype dt, double* y, void* stream) {
+  reset_launch_count();
+  if (!x || !w || !y || N <= 0 || C <= 0 || K <= 0 || (pad != 0 && pad != 1)) return set_last_error("bad argument"), WINO_E_ARG;
+  const int Ho = H + 2 * pad - 2, Wo = W + 2 * pad - 2;
+  if (Ho <= 0 || Wo <= 0) return set_last_error("bad geometry"), WINO_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  dim3 grid((Wo + 31) / 32, N * Ho, (K + 31) / 32);
+  switch (dt) {
+    case WINO_F32:
+      direct_f64_kernel<WINO_F32><<<grid, 256, 0, st>>>((const float*)x, (const float*)w, C, H, W, K, pad, Ho, Wo, y);
+      break;
+    case WINO_F16:
+      direct_f64_kernel<WINO_F16><<<grid, 256, 0, st>>>((const __half*)x, (const __half*)w, C, H, W, K, pad, Ho, Wo, y);
+      break;
+    case WINO_BF16:
+      direct_f64_kernel<WINO_BF16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)w, C, H, W,
+                                                         K, pad, Ho, Wo, y);
+      break;
+    default:
+      return set_last_error("bad dtype"), WINO_E_ARG;
+  }
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// transforms.cu -- the three CUDA-core stages of the Winograd layer
+// (Eq. 2: Y = A^T [(G g G^T) (.) (B^T d B)] A):
+//   K2 weight transform  U_u[k][c] = rd(slab_u(G g_{k,c} G^T))       (A1)
+//   K1 input transform   V_q[t][c] = rd((B^T d_{t,c} B)_q)           (A2)
+//   K4 output transform  y[n,k,..] = rd(A^T M_{t,k} A), ragged-clipped (A4)
+// All arithmetic is fp32 with the fp32-lowered exact matrices; rounding to the
+// storage dtype happens once per stored tensor (the "pipeline" model).
+#include <string>
+
+#include "transforms_impl.cuh"
+
+namespace wino {
+
+static InFn in_fn_(int dt, int m, int doff) {
+  const InFn(*t)[5] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
+  return t[m - 2][doff];
+}
+static OutFn out_fn_(int dt, int m, int doff) {
+  const OutFn(*t)[5] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
+  return t[m - 2][doff];
+}
+
+static bool md_ok(const wino_algo* al) { return al->m >= 2 && al->m <= 8 && al->D - al->m - 2 >= 0 && al->D - al->m - 2 <= 4; }
+
+wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* al, wino_dtype dt, void* U,
+                                 cudaStream_t st) {
+  Geo g = make_geo(al, 1, C, 3, 3, K, 1, dt);
+  size_t plane = (size_t)g.S * K * g.Cp;
+  dim3 grid((g.Cp + 127) / 128, K);
+  switch (dt) {
+    case WINO_F32:
+      weight_transform_kernel<WINO_F32><<<grid, 128, 0, st>>>((const float*)w, K, C, g.Cp, al->xp, al->ut,
+                                                              (float*)U, plane);
+      break;
+    case WINO_F16:
+      weight_transform_kernel<WINO_F16><<<grid, 128, 0, st>>>((const __half*)w, K, C, g.Cp, al->xp, al->ut,
+                                                              (__half*)U, plane);
+      break;
+    case WINO_BF16:
+      weight_transform_kernel<WINO_BF16><<<grid, 128, 0, st>>>((const __nv_bfloat16*)w, K, C, g.Cp, al->xp,
+                                                               al->ut, (__nv_bfloat16*)U, plane);
+      break;
+  }
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+wino_status run_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
+                                wino_dtype dt, wino_layout layout, void* V, cudaStream_t st) {
+  if (layout != WINO_NCHW || !md_ok(al)) {
+    set_last_error("input transform: unsupported layout / (m, domain)");
+    return WINO_E_UNSUPPORTED;
+  }
+  Geo g = make_geo(al, N, C, H, W, 1, pad, dt);
+  InArgs a{x, C, H, W, pad, g.th, g.tw, g.Cp, N, &al->xp, V, (size_t)g.T * g.Cp, (size_t)g.Q * g.T * g.Cp, st};
+  in_fn_(dt, al->m, al->D - al->m - 2)(a);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
+                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st) {
+  if (layout != WINO_NCHW || !md_ok(al)) {
+    set_last_error("output transform: unsupported layout / (m, domain)");
+    return WINO_E_UNSUPPORTED;
+  }
+  Geo g = make_geo(al, N, 1, H, W, K, pad, dt);
+  OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, g.Tp, &al->xp, y, st};
+  out_fn_(dt, al->m, al->D - al->m - 2)(a);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+}  // namespace wino

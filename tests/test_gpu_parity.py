@@ -1,0 +1,373 @@
+"""GPU parity: libwino's CUDA path (through the C ABI) against the CPU oracle.
+
+Bars:
+* every stage (U, V, M, y) element by element against the oracle's pipeline
+  model fed the same inputs, within the dtype rounding of fp32 values computed
+  in a different order (at most one dtype ulp apart plus fp32 slack);
+* the whole layer element by element against fp64 direct convolution within
+  the a-priori forward error bound of the pipeline model;
+* fp32: relative L1 <= 1e-4 (m <= 4), <= 1e-3 (m <= 8) (north star);
+* fp16 / bf16: mean per-tile relative error within +-10% of the oracle's
+  emulated error for the same algorithm and inputs, identical ranking;
+* 1D tiles in paper mode: bitwise equal to the oracle;
+* error statistics / fp64 direct kernels: 1e-12 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import paper_1905_05233_b200 as W
+from oracle import conv as CV
+from oracle import metrics as MT
+from oracle import precision as P
+from oracle import transforms as T
+
+pytestmark = pytest.mark.gpu
+
+TD = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}
+U_D = {"fp32": 2.0 ** -24, "fp16": 2.0 ** -11, "bf16": 2.0 ** -8}
+
+
+def dev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(TD[dtype]).cuda()
+
+
+def host(t):
+    return t.detach().float().cpu().numpy().astype(np.float64) if t.dtype != torch.float64 else t.cpu().numpy()
+
+
+def algo_pair(name, lowering="subsolver"):
+    mods, m = T.canonical(name)
+    spec = T.moduli_spec(mods)
+    a = W.WinoAlgo(spec, m, lowering=lowering)
+    ref = T.make_transforms(mods, m) if lowering == "subsolver" else T.residue_blocks(mods, m)
+    return a, ref, m
+
+
+def close_to_rounded(got, want, dtype, scale):
+    """got, want: dtype values of the same fp32 quantity computed in different
+    orders.  They may differ by one dtype ulp where the fp32 values straddle a
+    rounding boundary, plus the fp32 order difference itself (scale = the
+    magnitude bound of the summands)."""
+    tol = 2.0 * U_D[dtype] * np.abs(want) + 64 * 2.0 ** -24 * scale + 1e-30
+    bad = np.abs(got - want) > tol
+    assert not bad.any(), (int(bad.sum()), float(np.abs(got - want).max()))
+    return float((got == want).mean())
+
+
+# ------------------------------------------------------------------ stages
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("name,lowering", [("lin4", "subsolver"), ("sup1_4", "subsolver"), ("sup1_6", "residue"),
+                                           ("sup2_4", "residue"), ("lin8", "subsolver")])
+def test_weight_transform(dtype, name, lowering):
+    a, ref, m = algo_pair(name, lowering)
+    K, C = 24, 72
+    _, w = datagen.layer(1, C, K, 4, 4, dtype, seed=3)
+    U = W.wino_weight_transform(dev(w, dtype), a)
+    torch.cuda.synchronize()
+    if lowering == "subsolver":
+        Uo = P.pipeline_weight_transform(ref, w, dtype).reshape(a.units, K, C)
+        absG = np.abs(np.array([[float(v) for v in r] for r in ref.G]))
+    else:
+        _, Uo = P.pipeline_residue_weights(ref, w, dtype)
+        absG = np.abs(np.array([[float(v) for v in r] for r in ref.GP])) * 2
+    got = host(U[0]) + (host(U[1]) if dtype == "fp32" else 0)
+    scale = P.sep2(absG, np.abs(w).transpose(2, 3, 0, 1)).reshape(-1, K, C).max()
+    if dtype == "fp32":
+        assert np.abs(got[:, :, :C] - Uo).max() <= 2.0 ** -20 * scale
+    else:
+        close_to_rounded(got[:, :, :C], Uo, dtype, scale)
+    assert not got[:, :, C:].any()                      # channel padding is zero
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("name,lowering,pad", [("lin4", "subsolver", 1), ("sup1_6", "subsolver", 1),
+                                               ("lin3", "subsolver", 0), ("sup1_4", "residue", 1),
+                                               ("lin8", "subsolver", 1)])
+def test_input_transform(dtype, name, lowering, pad):
+    a, ref, m = algo_pair(name, lowering)
+    N, C, H, Wd = 2, 40, 19, 23
+    x, _ = datagen.layer(N, C, 1, H, Wd, dtype, seed=4)
+    V = W.wino_input_transform(dev(x, dtype), a, pad=pad)
+    torch.cuda.synchronize()
+    D = a.domain
+    if lowering == "subsolver":
+        Vo, _ = P.pipeline_input_transform(ref, x, dtype, pad)
+        absBT = np.abs(np.array([[float(v) for v in r] for r in ref.BT]))
+    else:
+        BPT = P.lower_f32([list(r) for r in zip(*ref.BP)])
+        d, _ = P.halo_tiles(np.asarray(x, np.float32), m, m + 2, pad)
+        Vo = P.rd(dtype, P.sep2(BPT, d)).transpose(0, 1, 2, 4, 5, 3).reshape(D, D, -1, C)
+        absBT = np.abs(BPT.astype(np.float64))
+    Vo = Vo.reshape(D * D, -1, C)
+    got = host(V[0]) + (host(V[1]) if dtype == "fp32" else 0)
+    assert got.shape[1] == Vo.shape[1]
+    scale = (absBT.sum(1).max() ** 2) * np.abs(x).max()
+    if dtype == "fp32":
+        assert np.abs(got[:, :, :C] - Vo).max() <= 2.0 ** -20 * scale
+    else:
+        frac = close_to_rounded(got[:, :, :C], Vo, dtype, scale)
+        assert frac > 0.99
+    assert not got[:, :, C:].any()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name,lowering,T_,C,K", [("lin4", "subsolver", 300, 136, 72),
+                                                  ("lin2", "subsolver", 129, 64, 256),
+                                                  ("sup1_4", "residue", 257, 70, 40),
+                                                  ("lin4", "subsolver", 1000, 512, 512)])
+def test_domain_gemm_isolated(dtype, name, lowering, T_, C, K):
+    """Feed identical U, V (oracle-made, dtype values) to the tensor-core GEMM."""
+    a, ref, m = algo_pair(name, lowering)
+    rng = np.random.default_rng(7)
+    Q, S = a.domain ** 2, a.units
+    Cp = -(-C // 64) * 64
+    Vh = np.zeros((1, Q, T_, Cp))
+    Uh = np.zeros((1, S, K, Cp))
+    Vh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, T_, C)), dtype)
+    Uh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, S, K, C)), dtype)
+    M = W.wino_domain_gemm(dev(Vh, dtype), dev(Uh, dtype), a, C, K)
+    torch.cuda.synchronize()
+    got = host(M)[:, :, :T_]
+    out_pt, in_pt, *_ = a.unit_table()
+    want = np.zeros((Q, K, T_))
+    aw = np.zeros((Q, K, T_))
+    for u in range(S):
+        want[out_pt[u]] += Uh[0, u] @ Vh[0, in_pt[u]].T
+        aw[out_pt[u]] += np.abs(Uh[0, u]) @ np.abs(Vh[0, in_pt[u]]).T
+    # fp32 accumulation of exact products: |err| <= gamma_n * sum |u v|
+    n = C * max(1, S // Q)
+    assert (np.abs(got - want) <= 1.01 * n * 2.0 ** -24 * aw + 1e-30).all()
+
+
+def test_domain_gemm_tf32x3():
+    """fp32 path: U, V made by the library (hi/lo planes); M vs fp64 products."""
+    a, ref, m = algo_pair("lin4")
+    x, w = datagen.layer(1, 96, 48, 14, 18, "fp32", seed=5)
+    xd, wd = dev(x, "fp32"), dev(w, "fp32")
+    U = W.wino_weight_transform(wd, a)
+    V = W.wino_input_transform(xd, a)
+    M = W.wino_domain_gemm(V, U, a, 96, 48)
+    torch.cuda.synchronize()
+    Uf = (host(U[0]) + host(U[1]))[:, :, :96]
+    Vf = (host(V[0]) + host(V[1]))[:, :, :96]
+    T_ = Vf.shape[1]
+    want = np.einsum("qkc,qtc->qkt", Uf, Vf)
+    aw = np.einsum("qkc,qtc->qkt", np.abs(Uf), np.abs(Vf))
+    got = host(M)[:, :, :T_]
+    assert (np.abs(got - want) <= (96 * 2.0 ** -24 + 2.0 ** -20) * aw + 1e-30).all()
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("name,lowering", [("lin4", "subsolver"), ("sup1_6", "subsolver"), ("sup1_4", "residue")])
+def test_output_transform(dtype, name, lowering):
+    a, ref, m = algo_pair(name, lowering)
+    N, K, H, Wd = 2, 20, 17, 13
+    Ho, Wo, th, tw = CV.tile_grid(H, Wd, m, 1)
+    T_ = N * th * tw
+    rng = np.random.default_rng(8)
+    D = a.domain
+    Mh = rng.standard_normal((D * D, K, T_)).astype(np.float32)
+    Md = torch.zeros((D * D, K, -(-T_ // 4) * 4), dtype=torch.float32)
+    Md[:, :, :T_] = torch.from_numpy(Mh)
+    y = W.wino_output_transform(Md.cuda(), a, N, K, H, Wd, 1, dtype)
+    torch.cuda.synchronize()
+    AT = P.lower_f32(ref.AT if lowering == "subsolver" else [list(r) for r in zip(*ref.AP)])
+    Yt = P.rd(dtype, P.sep2(AT, Mh.reshape(D, D, K, T_)))
+    want = P._scatter_tiles(Yt, N, K, th, tw, m, Ho, Wo)
+    scale = np.abs(AT).sum(1).max() ** 2 * np.abs(Mh).max()
+    close_to_rounded(host(y), want.astype(np.float64), dtype, scale)
+
+
+# ------------------------------------------------------------------ whole layer
+
+
+def _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad, xdist="relu_normal", seed=0):
+    a, ref, m = algo_pair(name, lowering)
+    x, w = datagen.layer(N, C, K, H, Wd, dtype, seed=seed, xdist=xdist)
+    y = W.wino_conv2d(dev(x, dtype), dev(w, dtype), a, pad=pad)
+    assert W.wino_last_launch_count() == 4
+    torch.cuda.synchronize()
+    yg = host(y)
+    yref = CV.direct_conv2d_f64(x, w, pad)
+    if lowering == "subsolver":
+        yo = P.pipeline_conv2d(ref, x, w, dtype, pad)
+        bound = P.elementwise_bound(ref, x, w, dtype, yref, pad, mma_rel=2.0 ** -20 if dtype == "fp32" else 0.0)
+        bad = np.abs(yg - yref) > bound
+        assert not bad.any(), (int(bad.sum()), float(np.abs(yg - yref).max()))
+    else:
+        yo = P.pipeline_residue_conv2d(ref, x, w, dtype, pad)
+    sg = MT.summary(MT.stats8(yg, yref, m))
+    so = MT.summary(MT.stats8(yo, yref, m))
+    return sg, so, m
+
+
+LAYER_CASES = [
+    ("lin2", "subsolver", 1, 8, 8, 16, 16, 1),          # cfg1 shape
+    ("sup1_2", "subsolver", 1, 8, 8, 16, 16, 1),
+    ("sup1_3", "subsolver", 1, 8, 8, 16, 16, 1),        # cfg1's literal {a, a+1, a^2+1, inf}
+    ("lin4", "subsolver", 2, 72, 40, 19, 23, 1),        # ragged everywhere, C not a multiple of 64
+    ("sup1_4", "subsolver", 2, 72, 40, 19, 23, 0),
+    ("lin6", "subsolver", 1, 128, 136, 30, 30, 1),
+    ("sup1_6", "subsolver", 1, 128, 136, 30, 30, 1),
+    ("lin8", "subsolver", 1, 64, 64, 26, 26, 1),
+    ("sup1_8", "subsolver", 1, 64, 64, 26, 26, 1),
+    ("sup2_6", "subsolver", 1, 64, 64, 26, 26, 1),
+    ("sup1_4", "residue", 2, 72, 40, 19, 23, 1),
+    ("sup1_6", "residue", 1, 128, 136, 30, 30, 1),
+    ("sup2_4", "residue", 1, 64, 48, 20, 20, 1),
+]
+
+
+@pytest.mark.parametrize("case", LAYER_CASES, ids=lambda c: f"{c[0]}-{c[1]}-C{c[3]}K{c[4]}-{c[5]}x{c[6]}p{c[7]}")
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+def test_layer(case, dtype):
+    name, lowering, N, C, K, H, Wd, pad = case
+    sg, so, m = _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad)
+    if dtype == "fp32":
+        assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3), sg
+    elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
+    assert sg["nonfinite"] == so["nonfinite"]
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_ranking_linear_vs_superlinear(dtype):
+    """Ratio-matched pair: F(6x6)+a^2+1 is more accurate than TC F(4x4), on
+    the GPU exactly as in the oracle, and within +-10% of it."""
+    errs_g, errs_o = {}, {}
+    for name in ("lin4", "sup1_6"):
+        sg, so, _ = _layer_check(name, "subsolver", dtype, 2, 128, 64, 28, 28, 1, seed=11)
+        errs_g[name], errs_o[name] = sg["mean_rel"], so["mean_rel"]
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10
+    assert (errs_g["sup1_6"] < errs_g["lin4"]) == (errs_o["sup1_6"] < errs_o["lin4"]) == True  # noqa: E712
+
+
+def test_edge_cases():
+    # single output pixel, single channel, pad 0
+    for (N, C, K, H, Wd, pad) in [(1, 1, 1, 3, 3, 0), (1, 1, 1, 1, 1, 1), (3, 3, 64, 9, 5, 1), (1, 130, 17, 6, 40, 1)]:
+        sg, so, m = _layer_check("lin4", "subsolver", "fp32", N, C, K, H, Wd, pad, xdist="uniform01")
+        assert sg["rel_l1"] <= 1e-4
+
+
+def test_fp16_overflow_is_counted_not_an_error():
+    a, ref, m = algo_pair("lin8")
+    rng = np.random.default_rng(2)
+    x = datagen.to_dtype_values(300.0 * rng.standard_normal((1, 16, 20, 20)), "fp16")
+    w = datagen.to_dtype_values(rng.standard_normal((8, 16, 3, 3)), "fp16")
+    y = W.wino_conv2d(dev(x, "fp16"), dev(w, "fp16"), a)
+    torch.cuda.synchronize()
+    yg = host(y)
+    yo = P.pipeline_conv2d(ref, x, w, "fp16")
+    ng, no = int((~np.isfinite(yg)).sum()), int((~np.isfinite(yo)).sum())
+    assert no > 0 and abs(ng - no) <= max(2, 0.02 * no)
+
+
+# ------------------------------------------------------------------ 1D tiles (cfg 2)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("fam", ["lin", "sup1", "sup2"])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
+def test_conv1d_paper_mode_bitwise(dtype, fam, n):
+    mods, m = T.canonical(f"{fam}{n}")
+    ts = T.make_transforms(mods, m)
+    a = W.WinoAlgo(T.moduli_spec(mods), m)
+    Tn = (1 << 15) + 3
+    x, h = datagen.tiles1d(Tn, n, dtype, seed=n)
+    y = W.wino_conv1d_tiles(dev(x, dtype), dev(h, dtype), a, per_op_rounding=True)
+    torch.cuda.synchronize()
+    yo = P.paper_conv1d(ts, x, h, dtype)
+    g = host(y).astype(np.float32)
+    same = (g.view(np.uint32) == yo.astype(np.float32).view(np.uint32)) | (np.isnan(g) & np.isnan(yo))
+    assert same.all(), int((~same).sum())
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name", ["lin4", "sup1_6", "sup2_8"])
+def test_conv1d_pipeline_mode(dtype, name):
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    a = W.WinoAlgo(T.moduli_spec(mods), m)
+    x, h = datagen.tiles1d(1 << 14, m, dtype, seed=1)
+    y = W.wino_conv1d_tiles(dev(x, dtype), dev(h, dtype), a, per_op_rounding=False)
+    torch.cuda.synchronize()
+    yo = P.pipeline_conv1d(ts, x, h, dtype)
+    ref = np.stack([sum(h[:, k] * x[:, j + k] for k in range(3)) for j in range(m)], 1)
+    eg, eo = MT.tile_rel_1d(host(y), ref).mean(), MT.tile_rel_1d(yo, ref).mean()
+    assert abs(eg / eo - 1) <= 0.10
+
+
+# ------------------------------------------------------------------ metric path kernels
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_error_stats_kernel(dtype):
+    rng = np.random.default_rng(0)
+    N, K, Ho, Wo, m = 2, 5, 13, 11, 4
+    yref = rng.standard_normal((N, K, Ho, Wo))
+    y = datagen.to_dtype_values(yref + 1e-3 * rng.standard_normal(yref.shape), dtype)
+    y[0, 1, 3, 4] = np.inf
+    yref[1, 2, :4, :4] = 0
+    y[1, 2, :4, :4] = 0
+    s = W.wino_error_stats(dev(y, dtype), torch.from_numpy(yref).cuda(), m).cpu().numpy()
+    so = MT.stats8(y, yref, m)
+    assert s[5] == so[5] == 1 and s[6] == so[6] and s[7] == so[7]
+    fin = np.isfinite(so)
+    np.testing.assert_allclose(s[fin], so[fin], rtol=1e-12)
+    assert np.array_equal(np.isinf(s), np.isinf(so))
+
+
+def test_error_stats_deterministic():
+    rng = np.random.default_rng(1)
+    yref = rng.standard_normal((4, 64, 28, 28))
+    y = dev(yref + 1e-3, "fp32")
+    r = torch.from_numpy(yref).cuda()
+    a = W.wino_error_stats(y, r, 4).cpu().numpy()
+    b = W.wino_error_stats(y, r, 4).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+def test_direct_f64_kernel(dtype):
+    x, w = datagen.layer(2, 19, 37, 15, 70, dtype, seed=9)
+    for pad in (0, 1):
+        y = W.wino_direct_conv2d_f64(dev(x, dtype), dev(w, dtype), pad).cpu().numpy()
+        np.testing.assert_allclose(y, CV.direct_conv2d_f64(x, w, pad), rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled
+
+
+@pytest.mark.parametrize("cfg,name,dtype", [("cfg3", "lin4", "fp16"), ("cfg3", "sup1_6", "fp16"),
+                                            ("cfg5", "lin4", "bf16"), ("cfg5", "sup1_6", "bf16"),
+                                            ("cfg5", "lin4", "fp32")])
+def test_full_size_sampled(cfg, name, dtype):
+    """Full BASELINE size in the launch configuration bench.py times; the oracle
+    recomputes a sample of images (images are independent)."""
+    c = dict(datagen.CONFIGS[cfg])
+    a, ref, m = algo_pair(name)
+    x, w = datagen.layer(c["N"], c["C"], c["K"], c["H"], c["W"], dtype, seed=0, xdist=c["xdist"])
+    xd, wd = dev(x, dtype), dev(w, dtype)
+    y = W.wino_conv2d(xd, wd, a)
+    yr = W.wino_direct_conv2d_f64(xd, wd, 1)
+    sg = W.summary(W.wino_error_stats(y, yr, m))
+    torch.cuda.synchronize()
+    idx = [0, 1, c["N"] - 1]
+    xs = x[idx]
+    yo = P.pipeline_conv2d(ref, xs, w, dtype)
+    yref = CV.direct_conv2d_f64(xs, w, 1)
+    np.testing.assert_allclose(host(yr)[idx], yref, rtol=1e-12, atol=1e-12)
+    yg = host(y)[idx]
+    bound = P.elementwise_bound(ref, xs, w, dtype, yref, 1, mma_rel=2.0 ** -20 if dtype == "fp32" else 0.0)
+    assert (np.abs(yg - yref) <= bound).all()
+    so = MT.summary(MT.stats8(yo, yref, m))
+    ss = MT.summary(MT.stats8(yg, yref, m))
+    if dtype == "fp32":
+        assert sg["rel_l1"] <= 1e-4
+    else:
+        assert abs(ss["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (ss, so)
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.15, (sg, so)   # whole layer vs sample

@@ -223,8 +223,7 @@ def test_pipeline_fp32_meets_north_star_and_bound(name):
     y = P.pipeline_conv2d(ts, x, w, "fp32")
     s = MT.summary(MT.stats8(y, yref, m))
     assert s["rel_l1"] <= (1e-4 if m <= 4 else 1e-3)
-    S, gam, u_d = P.abs_bound_conv2d(ts, x, w, "fp32")
-    bound = 1.05 * ((2 * u_d + gam) * S + u_d * np.abs(yref))
+    bound = P.elementwise_bound(ts, x, w, "fp32", yref)
     assert (np.abs(y - yref) <= bound).all()
 
 
@@ -237,8 +236,7 @@ def test_pipeline_lowp_bound_and_ranking(dtype):
         mods, m = T.canonical(name)
         ts = T.make_transforms(mods, m)
         y = P.pipeline_conv2d(ts, x, w, dtype)
-        S, gam, u_d = P.abs_bound_conv2d(ts, x, w, dtype)
-        bound = 1.05 * ((2 * u_d + gam) * S + u_d * np.abs(yref))
+        bound = P.elementwise_bound(ts, x, w, dtype, yref)
         assert (np.abs(y - yref) <= bound).all()
         errs[name] = MT.summary(MT.stats8(y, yref, m))["mean_rel"]
     assert errs["sup1_6"] < errs["lin4"]          # P:596 direction at ratio 2.25
