@@ -17,9 +17,13 @@
 //               buffered so the epilogue of item i overlaps the MMAs of i+1).
 //               kind::f16 for fp16/bf16; fp32 runs three kind::tf32 products
 //               hi*hi + hi*lo + lo*hi per K step (hi/lo planes made by K1/K2).
-//   warps 4..7  epilogue: tcgen05.ld 32x32b (TMEM lane = tile t) and
-//               coalesced stores of M[p][k][t] (a warp writes 128 contiguous
-//               bytes per k).
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (TMEM lane = tile t) into
+//               registers, st.shared into a [32 k][128 t] staging buffer
+//               (conflict-free: a warp writes 128 contiguous bytes per k), then
+//               one thread TMA-stores the box to M[p][k0:k0+32][t0:t0+128]
+//               (cp.async.bulk.tensor, clipped at the ragged edges).  The
+//               accumulator is released to the MMA warp as soon as its last
+//               columns are in registers.
 #include <string>
 
 #include "device.cuh"
@@ -39,18 +43,21 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int EPI_BUFS = 2;
+  static constexpr int EPI_BYTES = 32 * kBM * 4;   // one [32 k][128 t] fp32 box
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BUFS * EPI_BYTES + 1024 + 256;
 };
 
 template <bool kTF32, int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     domain_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
-                       float* __restrict__ Mout, int T, int K, int Tp, int Cp, int nMB, int nNB, int Q, int S,
+                       const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB, int nNB, int Q, int S,
                        uint32_t idesc, const __grid_constant__ GemmSched gs) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -60,6 +67,7 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmV);
     tma_prefetch(&tmU);
+    tma_prefetch(&tmM);
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
     fence_barrier_init();
@@ -139,30 +147,39 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // -------------------------------------------------- epilogue
     const int wq = warp & 3;
-    int acc = 0;
+    const bool storer = (warp == 4 && lane == 0);
+    int acc = 0, chunk = 0;
     uint32_t acc_phase = 0;
     for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
       const int nb = item % nNB, mb = (item / nNB) % nMB, p = item / (nNB * nMB);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int t = mb * kBM + wq * 32 + lane;
-      float* out = Mout + ((size_t)p * K + (size_t)nb * BN) * Tp + t;
-      const int kmax = min(BN, K - nb * BN);
 #pragma unroll 1
       for (int j0 = 0; j0 < BN; j0 += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
-        if (t < T) {
-#pragma unroll
-          for (int jj = 0; jj < 32; ++jj)
-            if (j0 + jj < kmax) out[(size_t)(j0 + jj) * Tp] = v[jj];
+        if (j0 + 32 == BN) {  // accumulator fully read: hand it back to the MMA warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (nb * BN + j0 >= K) continue;                 // columns past K (uniform branch)
+        float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
+        if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();   // the store that last read `buf` is done
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
+        fence_proxy_async_shared();
+        named_bar_sync(1, 128);
+        if (storer) {
+          tma_store_3d(&tmM, buf, mb * kBM, nb * BN + j0, p);
+          bulk_commit();
+        }
+        ++chunk;
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == 2) acc = 0, acc_phase ^= 1;
     }
+    if (storer) bulk_wait_all();
   }
   __syncthreads();
   if (warp == 2) {
@@ -189,16 +206,18 @@ static EncodeFn get_encode() {
   return fn;
 }
 
+// 3D tensor map; d0 innermost.  row0 = elements per d0-row in memory (>= d0).
 static bool make_map3(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, uint64_t d0,
-                      uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1) {
+                      uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1, bool swizzle = true, uint64_t row0 = 0) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
+  if (!row0) row0 = d0;
   cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * es, d0 * d1 * es};
+  cuuint64_t strides[2] = {row0 * es, row0 * d1 * es};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -214,7 +233,7 @@ static int num_sms() {
 }
 
 template <bool kTF32, int BN, int STAGES>
-static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, float* M, const Geo& g,
+static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
                                const GemmSched& gs, uint32_t fmt, cudaStream_t st) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
   auto kern = domain_gemm_kernel<kTF32, BN, STAGES>;
@@ -226,7 +245,7 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, flo
   const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
   const int items = g.Q * nMB * nNB;
   const int grid = items < num_sms() ? items : num_sms();
-  kern<<<grid, 256, Cfg::SMEM, st>>>(tv, tu, M, g.T, g.K, g.Tp, g.Cp, nMB, nNB, g.Q, g.S,
+  kern<<<grid, 256, Cfg::SMEM, st>>>(tv, tu, tm, g.T, g.K, g.Cp, nMB, nNB, g.Q, g.S,
                                      make_idesc(fmt, kBM, BN), gs);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
@@ -240,21 +259,22 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   int BN = tf32 ? (g.K > 64 ? 128 : 64) : (g.K > 128 ? 256 : (g.K > 64 ? 128 : 64));
   const uint32_t BK = 128 / (uint32_t)g.es;
-  CUtensorMap tv, tu;
+  CUtensorMap tv, tu, tm;
   if (!make_map3(&tv, cdt, g.es, V, g.Cp, g.T, (uint64_t)g.Q * g.planes, BK, kBM) ||
-      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN)) {
+      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
+      !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, g.T, g.K, g.Q, kBM, 32, false, g.Tp)) {
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
     return WINO_E_CUDA;
   }
   // UMMA operand formats: kind::f16 F16 = 0, BF16 = 1; kind::tf32 TF32 = 2.
   const uint32_t fmt = dt == WINO_F16 ? 0u : dt == WINO_BF16 ? 1u : 2u;
   if (tf32) {
-    if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, M, g, al->gs, fmt, st);
-    return launch_gemm<true, 64, 4>(tv, tu, M, g, al->gs, fmt, st);
+    if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, st);
+    return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, st);
   }
-  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, M, g, al->gs, fmt, st);
-  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, M, g, al->gs, fmt, st);
-  return launch_gemm<false, 64, 8>(tv, tu, M, g, al->gs, fmt, st);
+  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, st);
+  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, st);
+  return launch_gemm<false, 64, 8>(tv, tu, tm, g, al->gs, fmt, st);
 }
 
 }  // namespace wino
