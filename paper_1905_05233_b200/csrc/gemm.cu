@@ -28,6 +28,7 @@
 
 #include "device.cuh"
 #include "geometry.hpp"
+#include "tmap.hpp"
 
 namespace wino {
 
@@ -189,37 +190,6 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ------------------------------------------------------------------ host side
-
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeFn get_encode() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeFn>(p);
-  }
-  return fn;
-}
-
-// 3D tensor map; d0 innermost.  row0 = elements per d0-row in memory (>= d0).
-static bool make_map3(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, uint64_t d0,
-                      uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1, bool swizzle = true, uint64_t row0 = 0) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  if (!row0) row0 = d0;
-  cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {row0 * es, row0 * d1 * es};
-  cuuint32_t box[3] = {b0, b1, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return enc(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 static int num_sms() {
   static int n = 0;

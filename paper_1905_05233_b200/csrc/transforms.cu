@@ -12,20 +12,54 @@
 namespace wino {
 
 static InFn in_fn_(int dt, int m, int doff) {
-  const InFn(*t)[5] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
+  const InFn(*t)[3] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
   return t[m - 2][doff];
 }
 static OutFn out_fn_(int dt, int m, int doff) {
-  const OutFn(*t)[5] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
+  const OutFn(*t)[3] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
   return t[m - 2][doff];
 }
 
-static bool md_ok(const wino_algo* al) { return al->m >= 2 && al->m <= 8 && al->D - al->m - 2 >= 0 && al->D - al->m - 2 <= 4; }
+static bool md_ok(const wino_algo* al) { return al->m >= 2 && al->m <= 8 && al->D - al->m - 2 >= 0 && al->D - al->m - 2 <= 2; }
+
+template <int DT, int D>
+static void launch_wpts(const void* w, int K, int C, int Cp, const XformParams& xp, void* U, size_t plane,
+                        cudaStream_t st) {
+  using TT = typename DType<DT>::T;
+  weight_transform_points<DT, D><<<dim3(Cp / 64, (K + 3) / 4), dim3(32, 4), 0, st>>>((const TT*)w, K, C, Cp, xp,
+                                                                                    (TT*)U, plane);
+}
+template <int DT>
+static bool weight_points(int D, const void* w, int K, int C, int Cp, const XformParams& xp, void* U, size_t plane,
+                          cudaStream_t st) {
+  switch (D) {
+    case 4: launch_wpts<DT, 4>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 5: launch_wpts<DT, 5>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 6: launch_wpts<DT, 6>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 7: launch_wpts<DT, 7>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 8: launch_wpts<DT, 8>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 9: launch_wpts<DT, 9>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 10: launch_wpts<DT, 10>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 11: launch_wpts<DT, 11>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 12: launch_wpts<DT, 12>(w, K, C, Cp, xp, U, plane, st); return true;
+    default: return false;
+  }
+}
 
 wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* al, wino_dtype dt, void* U,
                                  cudaStream_t st) {
   Geo g = make_geo(al, 1, C, 3, 3, K, 1, dt);
   size_t plane = (size_t)g.S * K * g.Cp;
+  if (al->lowering == WINO_LOWER_SUBSOLVER && al->units == al->D * al->D) {
+    // units are the D x D Winograd points in row-major order (identity schedule)
+    const bool ok = dt == WINO_F32   ? weight_points<WINO_F32>(al->D, w, K, C, g.Cp, al->xp, U, plane, st)
+                    : dt == WINO_F16 ? weight_points<WINO_F16>(al->D, w, K, C, g.Cp, al->xp, U, plane, st)
+                                     : weight_points<WINO_BF16>(al->D, w, K, C, g.Cp, al->xp, U, plane, st);
+    if (ok) {
+      WINO_LAUNCH_CHECK();
+      return WINO_OK;
+    }
+  }
   dim3 grid((g.Cp + 127) / 128, K);
   switch (dt) {
     case WINO_F32:

@@ -1,15 +1,16 @@
 // transforms_impl.cuh -- kernels of transforms.cu (see there), instantiated
 // per storage dtype by xform_f32.cu / xform_f16.cu / xform_bf16.cu.
 #pragma once
+#include <cstdlib>
 #include <string>
+#include <type_traits>
 
 #include "device.cuh"
 #include "geometry.hpp"
+#include "tmap.hpp"
 
 namespace wino {
 
-// tiles per CTA row block of K1: about 32 output columns per CTA
-__host__ __device__ constexpr int k1_tjb(int M) { return M >= 8 ? 4 : (32 / M); }
 
 // ------------------------------------------------------------------ K2 weight transform
 // One thread per (k, c); c < Cp (zero padding for c >= C).  For the SUBSOLVER
@@ -55,177 +56,539 @@ __global__ void __launch_bounds__(128) weight_transform_kernel(const typename DT
   }
 }
 
-// B^T d B for one (tile, channel): d is the n_x x n_x halo in shared memory
-// (row stride `ld`); rowT = d B (per input row), V = B^T rowT, rounded once.
-template <int DT, int M, int NX, int D>
-__device__ __forceinline__ void tile_transform(const float* sd, int ld, const XformParams& xp,
-                                               typename DType<DT>::T* out, size_t qstride, size_t plane) {
-  using Tr = DType<DT>;
-  float rowT[NX][D];
-#pragma unroll
-  for (int r = 0; r < NX; ++r) {
-    float d[NX];
-#pragma unroll
-    for (int q = 0; q < NX; ++q) d[q] = sd[r * ld + q];
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-      float acc = 0.f;
-#pragma unroll
-      for (int q = 0; q < NX; ++q) acc = fmaf(xp.BT[j][q], d[q], acc);
-      rowT[r][j] = acc;
-    }
+template <int DT>
+__device__ __forceinline__ void store_pair(typename DType<DT>::T* dst, float2 v, size_t plane) {
+  if constexpr (DT == WINO_F32) {
+    float h0, l0, h1, l1;
+    split_tf32(v.x, h0, l0);
+    split_tf32(v.y, h1, l1);
+    *reinterpret_cast<float2*>(dst) = make_float2(h0, h1);
+    *reinterpret_cast<float2*>(dst + plane) = make_float2(l0, l1);
+  } else if constexpr (DT == WINO_F16) {
+    *reinterpret_cast<__half2*>(dst) = __float22half2_rn(v);
+  } else {
+    *reinterpret_cast<__nv_bfloat162*>(dst) = __float22bfloat162_rn(v);
   }
+}
+
+// SUBSOLVER fast path: U_{ij}[k][c] = (G g G^T)_{ij} for a channel pair per
+// lane (packed FFMA2, 128-byte coalesced stores per warp and point).
+// block (32, 4): x = channel pair within a 64-channel block, y = k offset.
+template <int DT, int D>
+__global__ void __launch_bounds__(128) weight_transform_points(const typename DType<DT>::T* __restrict__ w, int K,
+                                                               int C, int Cp, const __grid_constant__ XformParams xp,
+                                                               typename DType<DT>::T* __restrict__ U, size_t plane) {
+  using Tr = DType<DT>;
+  const int ca = blockIdx.x * 64 + 2 * threadIdx.x, cb = ca + 1;
+  const int k = blockIdx.y * 4 + threadIdx.y;
+  if (k >= K) return;
+  float2 g[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      g[a][b] = make_float2(ca < C ? Tr::load(w + ((size_t)k * C + ca) * 9 + a * 3 + b) : 0.f,
+                            cb < C ? Tr::load(w + ((size_t)k * C + cb) * 9 + a * 3 + b) : 0.f);
+  typename Tr::T* out = U + (size_t)k * Cp + ca;
+  const size_t ps = (size_t)K * Cp;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
+    float2 row[3];   // (G g)_{i,b}
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      float2 acc = __fmul2_rn(g[0][b], make_float2(xp.G[i][0], xp.G[i][0]));
+      acc = __ffma2_rn(g[1][b], make_float2(xp.G[i][1], xp.G[i][1]), acc);
+      row[b] = __ffma2_rn(g[2][b], make_float2(xp.G[i][2], xp.G[i][2]), acc);
+    }
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-      float acc = 0.f;
-#pragma unroll
-      for (int r = 0; r < NX; ++r) acc = fmaf(xp.BT[i][r], rowT[r][j], acc);
-      const size_t off = (size_t)(i * D + j) * qstride;
-      if constexpr (DT == WINO_F32) {
-        float hi, lo;
-        split_tf32(acc, hi, lo);
-        out[off] = hi;
-        out[off + plane] = lo;
-      } else {
-        out[off] = Tr::cvt(acc);
-      }
+      float2 acc = __fmul2_rn(row[0], make_float2(xp.G[j][0], xp.G[j][0]));
+      acc = __ffma2_rn(row[1], make_float2(xp.G[j][1], xp.G[j][1]), acc);
+      acc = __ffma2_rn(row[2], make_float2(xp.G[j][2], xp.G[j][2]), acc);
+      store_pair<DT>(out + (size_t)(i * D + j) * ps, acc, plane);
     }
   }
 }
 
 // ------------------------------------------------------------------ K1 input transform (NCHW)
-// CTA = (tile-column block of TJB tiles, (n, ti), 32 channels).  The halo rows
-// [ti*m - pad, ti*m - pad + nx) x [tj0*m - pad, ..) of 32 channels are staged in
-// shared memory (fp32, zero outside the image), then thread (c, tj) applies
-// B^T (.) B separably: rowT = d B (per input row), V = B^T rowT.  A warp holds
-// 32 consecutive channels of one tile, so each V_q store is one contiguous
-// 64 B (16-bit) / 128 B (fp32) segment of the K-major GEMM operand.
-template <int DT, int M, int NX, int D>
-__global__ void __launch_bounds__(32 * k1_tjb(M)) input_transform_nchw(
-    const typename DType<DT>::T* __restrict__ x, int C, int H, int W, int pad, int th, int tw, int Cp,
-    const __grid_constant__ XformParams xp, typename DType<DT>::T* __restrict__ V, size_t qstride, size_t plane) {
-  using Tr = DType<DT>;
-  constexpr int TJB = k1_tjb(M);
-  constexpr int SEG = TJB * M + NX - M;
-  constexpr int CS = (NX * SEG) | 1;  // odd channel stride: conflict-free smem reads
-  __shared__ float s[32 * CS];
-  const int tj0 = blockIdx.x * TJB;
-  const int n = blockIdx.y / th, ti = blockIdx.y % th;
-  const int c0 = blockIdx.z * 32;
-  const int row0 = ti * M - pad, col0 = tj0 * M - pad;
-  // halo load: one warp per (channel, row) segment, lanes along the row
-  // (coalesced); batches of RB rows per warp are loaded into registers before
-  // any is stored, so each thread keeps RB * EPL loads in flight.
-  {
-    constexpr int ROWS = 32 * NX;
-    constexpr int RPW = (ROWS + TJB - 1) / TJB;   // rows per warp
-    constexpr int EPL = (SEG + 31) / 32;          // elements per lane per row
-    constexpr int RB = RPW < 16 ? RPW : 16;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Channel-pair design for sm_100a.  CTA = (tile-column block of TJB tiles,
+// (n, tile row ti), 64-channel block); lane l of every warp owns the channel
+// pair (c0 + 2l, c0 + 2l + 1), so
+//  * the halo is staged in shared memory as float2 pairs s[row][col][l]
+//    (conflict-free 8-byte accesses), loaded with VEC-element vector loads
+//    along w and converted to fp32 once;
+//  * the separable transform V = B^T d B runs on packed FFMA2 (fma.rn.f32x2,
+//    one instruction for both channels, coefficient broadcast);
+//  * each V_q store of a warp is 32 x (2 channels) = one contiguous 128-byte
+//    row (16-bit; fp32: 256 B per plane) of the K-major GEMM operand.
+// Warp w handles tiles tj0 + w, tj0 + w + nwarps, ...  The column stage is
+// chunked by JC output columns so the row-stage intermediates (NX x JC float2)
+// stay in registers at every m.
+// Stage NX halo rows of a channel pair per lane into s2[row][col][lane]
+// (float2 = (channel a, channel b)): zero fill outside the image, then
+// vectors of VEC elements along w (aligned in global coordinates) in batches
+// of LB, all loads of a batch issued before any is consumed.  Warp w stages
+// rows w, w + nw, ...
+template <int VEC, typename TT> struct VecT;
+template <typename TT> struct VecT<1, TT> { using T = TT; };
+template <int VEC, typename TT> struct VecT {
+  using T = typename std::conditional<VEC * sizeof(TT) == 16, uint4,
+            typename std::conditional<VEC * sizeof(TT) == 8, uint2, unsigned int>::type>::type;
+};
+template <typename Tr, int VEC, int NX>
+__device__ __forceinline__ void stage_halo(const typename Tr::T* xa, const typename Tr::T* xb, bool oka, bool okb,
+                                           int H, int W, int row0, int col0, int SEG, int qlo, int qhi, float2* s2,
+                                           int warp, int nw, int lane) {
+  using TT = typename Tr::T;
+  using VT = typename VecT<VEC, TT>::T;
+  constexpr int LB = 16 / (int)sizeof(VT) < 4 ? 4 : (16 / (int)sizeof(VT) > 8 ? 8 : 16 / (int)sizeof(VT));
+  const int v0 = qlo / VEC, nv = (qhi + VEC - 1) / VEC - v0;
 #pragma unroll 1
-    for (int i0 = 0; i0 < RPW; i0 += RB) {
-      float v[RB][EPL];
+  for (int a = warp; a < NX; a += nw) {
+    const int r = row0 + a;
+    float2* srow = s2 + a * SEG * 32 + lane;
+    if (r < 0 || r >= H) {
+      for (int b = 0; b < SEG; ++b) srow[b * 32] = make_float2(0.f, 0.f);
+      continue;
+    }
+    for (int b = 0; b < qlo - col0; ++b) srow[b * 32] = make_float2(0.f, 0.f);
+    for (int b = qhi - col0; b < SEG; ++b) srow[b * 32] = make_float2(0.f, 0.f);
+    const VT* ra = reinterpret_cast<const VT*>(xa + (size_t)r * W) + v0;
+    const VT* rb = reinterpret_cast<const VT*>(xb + (size_t)r * W) + v0;
+    float2* sv = srow + (v0 * VEC - col0) * 32;
+#pragma unroll 1
+    for (int vb = 0; vb < nv; vb += LB) {
+      VT ua[LB], ub[LB];
 #pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        const int rr = warp + (i0 + i) * TJB;
-        const int cl = rr / NX, a = rr - cl * NX;
-        const int r = row0 + a, c = c0 + cl;
-        const bool rowok = rr < ROWS && c < C && r >= 0 && r < H;
-        const typename Tr::T* src = x + (((size_t)n * C + c) * H + r) * W;
-#pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          const int q = col0 + lane + 32 * e;
-          v[i][e] = (rowok && lane + 32 * e < SEG && q >= 0 && q < W) ? Tr::load(src + q) : 0.f;
+      for (int k = 0; k < LB; ++k) {
+        ua[k] = VT{}, ub[k] = VT{};
+        if (vb + k < nv) {
+          if (oka) ua[k] = ra[vb + k];
+          if (okb) ub[k] = rb[vb + k];
         }
       }
 #pragma unroll
-      for (int i = 0; i < RB; ++i) {
-        const int rr = warp + (i0 + i) * TJB;
-        if (rr >= ROWS) break;
-        const int cl = rr / NX, a = rr - cl * NX;
+      for (int k = 0; k < LB; ++k) {
+        if (vb + k >= nv) break;
+        const int q0 = (v0 + vb + k) * VEC;
+        const TT* ea = reinterpret_cast<const TT*>(&ua[k]);
+        const TT* eb = reinterpret_cast<const TT*>(&ub[k]);
+        float2* dst = sv + (vb + k) * VEC * 32;
+        if (q0 >= qlo && q0 + VEC <= qhi) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e)
-          if (lane + 32 * e < SEG) s[cl * CS + a * SEG + lane + 32 * e] = v[i][e];
+          for (int j = 0; j < VEC; ++j) dst[j * 32] = make_float2(Tr::load(ea + j), Tr::load(eb + j));
+        } else {
+#pragma unroll
+          for (int j = 0; j < VEC; ++j)
+            if (q0 + j >= qlo && q0 + j < qhi) dst[j * 32] = make_float2(Tr::load(ea + j), Tr::load(eb + j));
+        }
       }
     }
   }
-  __syncthreads();
-  const int cl = threadIdx.x & 31, tjl = threadIdx.x >> 5;
-  const int tj = tj0 + tjl;
-  if (tj >= tw) return;
-  const size_t t = ((size_t)n * th + ti) * tw + tj;
-  tile_transform<DT, M, NX, D>(s + cl * CS + tjl * M, SEG, xp, V + t * Cp + c0 + cl, qstride, plane);
 }
 
-// Full-row variant: the CTA covers all tw tiles of tile-row (n, ti) for 32
-// channels, so each channel's halo is ONE contiguous range of x
-// (rows [ti*m - pad, ti*m - pad + nx) clipped to the image), read with
-// VEC-element vector loads (VEC * sizeof(T) = 8 or 16 bytes).
-template <int DT, int M, int NX, int D, int VEC>
-__global__ void __launch_bounds__(512) input_transform_rows(
-    const typename DType<DT>::T* __restrict__ x, int C, int H, int W, int pad, int th, int tw, int Cp,
+__host__ __device__ constexpr int k1_nchunk(int NX, int D) { return D * NX <= 36 ? 1 : (D * NX + 31) / 32; }
+__host__ __device__ constexpr int k1_jc(int NX, int D) { return (D + k1_nchunk(NX, D) - 1) / k1_nchunk(NX, D); }
+
+// V = B^T d B for one tile and the channel pair of this lane.  The halo row a
+// (a < NX) of the tile starts at ring + slot(a) * SEG * 32 + col * 32, slot(a)
+// = (s0 + a) mod NX (a ring of NX staged rows; s0 = 0 for a plain buffer).
+// The separable transform runs on packed FFMA2 (coefficient broadcast); each
+// V_q store of the warp is one contiguous 128-byte (16-bit) / 2 x 256-byte
+// (fp32 hi/lo) row of the K-major GEMM operand.
+template <int DT, int NX, int D>
+__device__ __forceinline__ void transform_tile_pairs(const float2* ring, int s0, int SEG, int col,
+                                                     const XformParams& xp, typename DType<DT>::T* out,
+                                                     size_t qstride, size_t plane) {
+  constexpr int JC = k1_jc(NX, D);
+  if constexpr (k1_nchunk(NX, D) == 1) {
+    // small tiles: everything unrolled (coefficients in uniform registers),
+    // in FJ-column chunks separated by a memory clobber so the scheduler
+    // cannot interleave them (D x FJ accumulators live, not D x D)
+    constexpr int FJ = NX * D > 24 ? (D + 1) / 2 : D;
+#pragma unroll
+    for (int j0 = 0; j0 < D; j0 += FJ) {
+      float2 acc[D][FJ];
+#pragma unroll
+      for (int a = 0; a < NX; ++a) {
+        const int sa = s0 + a < NX ? s0 + a : s0 + a - NX;
+        const float2* sd = ring + (sa * SEG + col) * 32;
+        float2 d[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) d[q] = sd[q * 32];
+#pragma unroll
+        for (int jj = 0; jj < FJ; ++jj) {
+          if (j0 + jj < D) {
+            float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < NX; ++q) {
+              const float c = xp.BT[j0 + jj][q];
+              rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+            }
+#pragma unroll
+            for (int i = 0; i < D; ++i) {
+              const float c = xp.BT[i][a];
+              acc[i][jj] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < FJ; ++jj)
+          if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+      asm volatile("" ::: "memory");
+    }
+  } else {
+    // larger tiles: JC output columns at a time and a rolled loop over input
+    // rows, so only D x JC accumulators and one halo row live in registers
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += JC) {
+      float2 acc[D][JC];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) acc[i][jj] = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int a = 0; a < NX; ++a) {
+        const int sa = s0 + a < NX ? s0 + a : s0 + a - NX;
+        const float2* sd = ring + (sa * SEG + col) * 32;
+        float2 d[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) d[q] = sd[q * 32];
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) {
+          float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < NX; ++q) {
+            const float c = xp.BT[j0 + jj < D ? j0 + jj : D - 1][q];
+            rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+          }
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const float c = xp.BT[i][a];
+            acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj)
+          if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K1 input transform (NCHW)
+// Channel-pair design for sm_100a.  Lane l of every warp owns the channel pair
+// (c0 + 2l, c0 + 2l + 1) of a 64-channel block; warp w transforms tiles
+// w, w + nwarps, ... of the CTA's TJB-tile column block; the halo is staged in
+// shared memory as float2 pairs ring[row][col][l] (fp32, conflict-free 8-byte
+// accesses).
+//
+// input_transform_tma (the main path): a CTA owns (tile-column block, image
+// n, channel block) and walks down all th tile rows.  One thread issues TMA
+// boxes of the m new input rows of each step (64 channels at once) into a ring
+// of NSLOT raw slots, NSLOT - 1 steps ahead of the math; completion is tracked
+// by per-slot mbarriers (no cp.async bookkeeping in the other threads).  Each
+// step converts its raw box into the packed ring[row][pair][col] (row pitch
+// SEGP odd: conflict-free for lane = channel pair), and the 2 halo rows shared
+// with the previous tile row are reused, so x is read from HBM once.
+//   mode 0 (flat): rows are whole image rows, box {RB * W, 64} of the
+//                  [N*C][H*W] view (any W with H*W*es % 16 == 0)
+//   mode 1 (3D):   box {BOXC, RB, 64} of the [N*C][H][W] view (W*es % 16 == 0)
+// TMA zero-fills rows / columns outside the image.
+template <int DT> struct PairT;
+template <> struct PairT<WINO_F32> {
+  using T = float2;
+  static __device__ __forceinline__ T pack(float a, float b) { return make_float2(a, b); }
+  static __device__ __forceinline__ float2 unpack(T v) { return v; }
+};
+template <> struct PairT<WINO_BF16> {
+  using T = uint32_t;   // (bf16 a, bf16 b): a in the low half
+  static __device__ __forceinline__ T pack(__nv_bfloat16 a, __nv_bfloat16 b) {
+    return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+  }
+  static __device__ __forceinline__ float2 unpack(T v) {
+    return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
+  }
+};
+template <> struct PairT<WINO_F16> {
+  using T = uint32_t;
+  static __device__ __forceinline__ T pack(__half a, __half b) {
+    return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+  }
+  static __device__ __forceinline__ float2 unpack(T v) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&v));
+  }
+};
+
+template <int DT, int NX, int D, typename PT>
+__device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int RR, int SEGP, int col,
+                                                    const XformParams& xp, typename DType<DT>::T* out,
+                                                    size_t qstride, size_t plane) {
+  using P = PairT<DT>;
+  constexpr int JC = k1_jc(NX, D);
+  if constexpr (k1_nchunk(NX, D) == 1) {
+    float2 acc[D][D];
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+      const int sa = s0 + a < RR ? s0 + a : s0 + a - RR;
+      const PT* sd = ring + sa * 32 * SEGP + col;
+      float2 d[NX];
+#pragma unroll
+      for (int q = 0; q < NX; ++q) d[q] = P::unpack(sd[q]);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+          const float c = xp.BT[j][q];
+          rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const float c = xp.BT[i][a];
+          acc[i][j] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
+  } else {
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += JC) {
+      float2 acc[D][JC];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) acc[i][jj] = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int a = 0; a < NX; ++a) {
+        const int sa = s0 + a < RR ? s0 + a : s0 + a - RR;
+        const PT* sd = ring + sa * 32 * SEGP + col;
+        float2 d[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) d[q] = P::unpack(sd[q]);
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) {
+          float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < NX; ++q) {
+            const float c = xp.BT[j0 + jj < D ? j0 + jj : D - 1][q];
+            rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+          }
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const float c = xp.BT[i][a];
+            acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj)
+          if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+    }
+  }
+}
+
+constexpr int K1_CONV_WARPS = 4;   // converter warps of input_transform_tma
+
+struct K1Geo {
+  int C, H, W, pad, th, tw, Cp, TJB;
+  int mode, RB, BOXC, NSLOT, RR, SEGP;
+  int ralign, calign;   // flat boxes start at a multiple of ralign rows, 3D boxes at a multiple of calign columns
+  unsigned box_bytes, slot_bytes;
+};
+
+template <int DT, int M, int NX, int D>
+__global__ void __launch_bounds__(352, 2) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
+                                                              const __grid_constant__ K1Geo gk,
+                                                              const __grid_constant__ XformParams xp,
+                                                              typename DType<DT>::T* __restrict__ V, size_t qstride,
+                                                              size_t plane) {
+  using Tr = DType<DT>;
+  using TT = typename Tr::T;
+  using P = PairT<DT>;
+  using PT = typename P::T;
+  extern __shared__ __align__(16) uint8_t k1_smem_raw[];
+  // TMA destinations must be 128-byte aligned: offset the shared array (stays a
+  // shared-space pointer, so accesses compile to LDS / STS)
+  uint8_t* k1_smem = k1_smem_raw + ((128u - (smem_u32(k1_smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(k1_smem);
+  uint8_t* raw = k1_smem + 128;
+  PT* ring = reinterpret_cast<PT*>(raw + (size_t)gk.NSLOT * gk.slot_bytes);
+  const int C = gk.C, W = gk.W, pad = gk.pad, th = gk.th, RR = gk.RR, SEGP = gk.SEGP, NSLOT = gk.NSLOT;
+  const int SEG = gk.TJB * M + NX - M;
+  const int tj0 = blockIdx.x * gk.TJB;
+  const int n = blockIdx.y;
+  const int c0 = blockIdx.z * 64;
+  const int col0 = tj0 * M - pad;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool leader = threadIdx.x == 0;
+  const int crow = n * C + c0;   // first channel row of the box in the [N*C] dimension
+
+  auto wait = [&](int it) {
+    const int s = (it + 1) % NSLOT;
+    mbar_wait(&full[s], (uint32_t)(((it + 1) / NSLOT) & 1));
+  };
+  // raw slot of step it -> packed ring rows; lanes walk ring columns b
+  // TMA boxes whose in-bounds part does not start on a 16-byte boundary of
+  // the row (negative or unaligned inner coordinates) trap as an illegal
+  // instruction (measured, scripts/tma_probe.cu), so boxes start at a
+  // non-negative, 16-byte aligned column / flat offset; the extra leading
+  // rows / columns are skipped here and rows / columns before the image are
+  // zeros.
+  const int cst = ((col0 < 0 ? 0 : col0) / gk.calign) * gk.calign;
+  // raw slot of step it -> packed ring rows (executed by the converter warps,
+  // one halo row each; lanes walk the ring columns)
+  const int cw = nw - K1_CONV_WARPS;     // compute warps
+  auto convert = [&](int it) {
+    const TT* rs = reinterpret_cast<const TT*>(raw + (size_t)((it + 1) % NSLOT) * gk.slot_bytes);
+    const int RBW = gk.mode == 0 ? gk.RB * W : gk.RB * gk.BOXC;   // elements per channel in the box
+    const int rstride = gk.mode == 0 ? W : gk.BOXC;
+    const int g0 = it * M - pad + NX - M;
+    const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
+    // ring columns [blo, bhi) are inside the image (the others stay zero)
+    const int blo = col0 < 0 ? -col0 : 0;
+    const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
+    const int qoff = gk.mode == 0 ? col0 : col0 - cst;   // raw column of ring column b: b + qoff
+    const bool allc = c0 + 64 <= C;                      // every channel of the block is real
+#pragma unroll 1
+    for (int k = warp - cw; k < M; k += nw - cw) {
+      const int g = g0 + k;
+      if (g < -pad) continue;
+      PT* drow = ring + ((g + 8 * RR) % RR) * 32 * SEGP;
+      const TT* rrow = rs + (g < 0 ? 0 : g - gst) * rstride + qoff;
+      if (g >= 0 && allc) {
+        for (int b = blo + lane; b < bhi; b += 32) {
+#pragma unroll 8
+          for (int p = 0; p < 32; ++p)
+            drow[p * SEGP + b] = P::pack(rrow[(2 * p) * RBW + b], rrow[(2 * p + 1) * RBW + b]);
+        }
+      } else {
+        for (int b = blo + lane; b < bhi; b += 32) {
+#pragma unroll 4
+          for (int p = 0; p < 32; ++p) {
+            const int ca = c0 + 2 * p;
+            const TT va = (g >= 0 && ca < C) ? rrow[(2 * p) * RBW + b] : Tr::cvt(0.f);
+            const TT vb = (g >= 0 && ca + 1 < C) ? rrow[(2 * p + 1) * RBW + b] : Tr::cvt(0.f);
+            drow[p * SEGP + b] = P::pack(va, vb);
+          }
+        }
+      }
+    }
+  };
+
+  if (leader) {
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    tma_prefetch(&tmx);
+  }
+  // ring columns before the image (and, for flat boxes, after it) stay zero
+  {
+    const int blo = col0 < 0 ? -col0 : 0;
+    const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
+    const PT z = P::pack(Tr::cvt(0.f), Tr::cvt(0.f));
+    for (int r = threadIdx.x; r < RR * 32; r += blockDim.x) {
+      PT* row = ring + r * SEGP;
+      for (int b = 0; b < blo; ++b) row[b] = z;
+      for (int b = bhi; b < SEG; ++b) row[b] = z;
+    }
+  }
+  __syncthreads();
+  // TMA of the m new rows of step `it` into raw slot (it + 1) % NSLOT (leader only;
+  // written out here rather than in a lambda so the tensor map stays a kernel
+  // parameter address)
+#define K1_ISSUE(it_)                                                                                    \
+  do {                                                                                                   \
+    const int s_ = ((it_) + 1) % NSLOT;                                                                  \
+    const int g0_ = gk.mode == 0 ? (max((it_) * M - pad + NX - M, 0) / gk.ralign) * gk.ralign                \
+                                 : max((it_) * M - pad + NX - M, 0);                                   \
+    fence_proxy_async_shared();                                                                          \
+    mbar_arrive_expect_tx(&full[s_], gk.box_bytes);                                                      \
+    if (gk.mode == 0) tma_load_2d(raw + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], g0_ * W, crow);     \
+    else tma_load_3d(raw + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], cst, g0_, crow);                 \
+  } while (0)
+  // warp specialisation: warps 0 .. cw-1 transform tiles, the K1_CONV_WARPS
+  // converter warps issue the TMA boxes (lane 0 of warp cw) and converts the raw rows of step ti+1
+  // while tile row ti is transformed; one CTA barrier per step.
+  const bool conv = warp >= cw;
+  if (conv) {
+    if (warp == cw && lane == 0)
+      for (int it = -1; it < NSLOT - 1 && it < th; ++it) K1_ISSUE(it);
+    __syncwarp();
+    wait(-1);
+    convert(-1);
+    wait(0);
+    convert(0);
+  }
+  __syncthreads();
+  const int ca = c0 + 2 * lane;
+#pragma unroll 1
+  for (int ti = 0; ti < th; ++ti) {
+    if (conv) {
+      if (warp == cw && lane == 0 && ti + NSLOT - 1 < th) K1_ISSUE(ti + NSLOT - 1);
+      __syncwarp();
+      if (ti + 1 < th) {
+        wait(ti + 1);
+        convert(ti + 1);
+      }
+    } else {
+      const int s0 = (ti * M - pad + 8 * RR) % RR;
+      for (int tjl = warp; tjl < gk.TJB; tjl += cw) {
+        const int tj = tj0 + tjl;
+        if (tj >= gk.tw) break;
+        const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
+        transform_tile_ring<DT, NX, D, PT>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + t * gk.Cp + ca,
+                                           qstride, plane);
+      }
+    }
+    __syncthreads();
+  }
+#undef K1_ISSUE
+}
+
+// Synchronous variant for rows whose vectors are narrower than 4 bytes (odd W
+// in 16-bit): CTA = (tile-column block, (n, ti), channel block).
+template <int DT, int M, int NX, int D>
+__global__ void __launch_bounds__(256, 2) input_transform_pairs(
+    const typename DType<DT>::T* __restrict__ x, int C, int H, int W, int pad, int th, int tw, int Cp, int TJB, int VEC,
     const __grid_constant__ XformParams xp, typename DType<DT>::T* __restrict__ V, size_t qstride, size_t plane) {
   using Tr = DType<DT>;
   using TT = typename Tr::T;
-  extern __shared__ float s_dyn[];
-  const int SEG = tw * M + NX - M;
-  const int CS = (NX * SEG) | 1;
+  extern __shared__ float2 s2[];
+  const int SEG = TJB * M + NX - M;   // staged columns
+  const int tj0 = blockIdx.x * TJB;
   const int n = blockIdx.y / th, ti = blockIdx.y % th;
-  const int c0 = blockIdx.z * 32;
-  const int r0 = ti * M - pad;
-  const int rlo = r0 < 0 ? 0 : r0, rhi = (r0 + NX > H) ? H : r0 + NX;
+  const int c0 = blockIdx.z * 64;
+  const int row0 = ti * M - pad, col0 = tj0 * M - pad;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // zero fill: left/right padding columns of every row, and rows outside the image
-  for (int e = threadIdx.x; e < 32 * NX; e += blockDim.x) {
-    const int cl = e / NX, a = e - cl * NX;
-    float* row = s_dyn + cl * CS + a * SEG;
-    const int r = r0 + a;
-    if (r < 0 || r >= H || c0 + cl >= C) {
-      for (int b = 0; b < SEG; ++b) row[b] = 0.f;
-    } else {
-      for (int b = 0; b < pad; ++b) row[b] = 0.f;
-      for (int b = pad + W; b < SEG; ++b) row[b] = 0.f;
-    }
-  }
-  const int nvec = (rhi - rlo) * W / VEC;
-  const float invW = 1.0f / (float)W;
-  for (int cl = warp; cl < 32; cl += nw) {
-    const int c = c0 + cl;
-    if (c >= C || nvec <= 0) continue;
-    const TT* src = x + (((size_t)n * C + c) * H + rlo) * W;
-    float* dst = s_dyn + cl * CS + (rlo - r0) * SEG + pad;
-    for (int e = lane; e < nvec; e += 32) {
-      const int flat = e * VEC;
-      int a = __float2int_rz(((float)flat + 0.5f) * invW);
-      a -= (a * W > flat);
-      a += ((a + 1) * W <= flat);
-      const int col = flat - a * W;
-      float v[VEC];
-      if constexpr (VEC * sizeof(TT) == 8) {
-        const uint2 u = __ldg(reinterpret_cast<const uint2*>(src + flat));
-        const TT* e2 = reinterpret_cast<const TT*>(&u);
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) v[k] = Tr::load(e2 + k);
-      } else if constexpr (VEC * sizeof(TT) == 16) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src + flat));
-        const TT* e2 = reinterpret_cast<const TT*>(&u);
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) v[k] = Tr::load(e2 + k);
-      } else {
-#pragma unroll
-        for (int k = 0; k < VEC; ++k) v[k] = Tr::load(src + flat + k);
-      }
-#pragma unroll
-      for (int k = 0; k < VEC; ++k) dst[a * SEG + col + k] = v[k];
-    }
+  const int ca = c0 + 2 * lane, cb = ca + 1;
+  const bool oka = ca < C, okb = cb < C;
+  const int qlo = col0 < 0 ? 0 : col0;
+  const int qhi = (col0 + SEG < W) ? col0 + SEG : W;  // in-image columns [qlo, qhi)
+  const TT* xa = x + ((size_t)n * C + (oka ? ca : 0)) * H * W;
+  const TT* xb = x + ((size_t)n * C + (okb ? cb : 0)) * H * W;
+  switch (VEC * (int)sizeof(TT)) {
+    case 16: stage_halo<Tr, 16 / (int)sizeof(TT), NX>(xa, xb, oka, okb, H, W, row0, col0, SEG, qlo, qhi, s2, warp, nw, lane); break;
+    case 8: stage_halo<Tr, 8 / (int)sizeof(TT), NX>(xa, xb, oka, okb, H, W, row0, col0, SEG, qlo, qhi, s2, warp, nw, lane); break;
+    case 4: stage_halo<Tr, 4 / (int)sizeof(TT), NX>(xa, xb, oka, okb, H, W, row0, col0, SEG, qlo, qhi, s2, warp, nw, lane); break;
+    default: stage_halo<Tr, 1, NX>(xa, xb, oka, okb, H, W, row0, col0, SEG, qlo, qhi, s2, warp, nw, lane); break;
   }
   __syncthreads();
-  const int cl = threadIdx.x & 31, tj = threadIdx.x >> 5;
-  if (tj >= tw) return;
-  const size_t t = ((size_t)n * th + ti) * tw + tj;
-  tile_transform<DT, M, NX, D>(s_dyn + cl * CS + tj * M, SEG, xp, V + t * Cp + c0 + cl, qstride, plane);
+  for (int tjl = warp; tjl < TJB; tjl += nw) {
+    const int tj = tj0 + tjl;
+    if (tj >= tw) break;
+    const size_t t = ((size_t)n * th + ti) * tw + tj;
+    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + t * Cp + ca, qstride, plane);
+  }
 }
 
 // ------------------------------------------------------------------ K4 output transform (NCHW)
@@ -318,23 +681,89 @@ using OutFn = void (*)(const OutArgs&);
 
 template <int DT, int M, int D>
 static void launch_in(const InArgs& a) {
-  using Tr = DType<DT>;
-  constexpr int VEC = 16 / (int)sizeof(typename Tr::T) / (sizeof(typename Tr::T) == 2 ? 2 : 1);  // 8 B (16-bit) / 16 B (fp32)
-  const int seg = a.tw * M + 2;
-  const size_t smem = (size_t)32 * ((M + 2) * seg | 1) * sizeof(float);
-  if (a.tw <= 16 && smem <= 160 * 1024 && a.W % VEC == 0 && (reinterpret_cast<uintptr_t>(a.x) % (VEC * sizeof(typename Tr::T))) == 0) {
-    auto kern = input_transform_rows<DT, M, M + 2, D, VEC>;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid(1, a.N * a.th, a.Cp / 32);
-    kern<<<grid, 32 * a.tw, smem, a.st>>>((const typename Tr::T*)a.x, a.C, a.H, a.W, a.pad, a.th, a.tw, a.Cp, *a.xp,
-                                          (typename Tr::T*)a.V, a.qstride, a.plane);
-    return;
+  using TT = typename DType<DT>::T;
+  using PT = typename PairT<DT>::T;
+  constexpr int NX = M + 2;
+  const size_t es = sizeof(TT);
+  const uintptr_t xa = reinterpret_cast<uintptr_t>(a.x);
+  const CUtensorMapDataType cdt = DT == WINO_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : DT == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  K1Geo gk{};
+  gk.C = a.C, gk.H = a.H, gk.W = a.W, gk.pad = a.pad, gk.th = a.th, gk.tw = a.tw, gk.Cp = a.Cp;
+  CUtensorMap tm;
+  bool ok = xa % 16 == 0;
+  if (ok && ((size_t)a.W * es) % 16 == 0) {
+    // 3D boxes {BOXC, M, 64} over column blocks of up to 8 tiles
+    gk.mode = 1;
+    gk.TJB = a.tw < 7 ? a.tw : 7;
+    const int al = (int)(16 / es);
+    gk.calign = al, gk.ralign = 1;
+    // box columns: the staged segment plus up to al - 1 leading columns of alignment
+    while (gk.TJB > 1 && ((gk.TJB * M + 2 + 2 * al - 2) / al) * al > 256) --gk.TJB;
+    gk.BOXC = ((gk.TJB * M + 2 + 2 * al - 2) / al) * al;
+    gk.RB = M;
+    const uint64_t dims[3] = {(uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.N * a.C};
+    const uint64_t str[2] = {(uint64_t)a.W * es, (uint64_t)a.H * a.W * es};
+    const uint32_t box[3] = {(uint32_t)gk.BOXC, (uint32_t)gk.RB, 64};
+    ok = make_map(&tm, cdt, 3, a.x, dims, str, box, false);
+    gk.box_bytes = (unsigned)(gk.BOXC * gk.RB * 64 * es);
+  } else if (ok && ((size_t)a.H * a.W * es) % 16 == 0) {
+    // whole image rows: flat boxes {RB * W, 64} of the [N*C][H*W] view
+    gk.mode = 0;
+    gk.TJB = a.tw;
+    int r16 = 1;
+    while ((r16 * a.W * es) % 16) ++r16;      // rows per 16-byte aligned flat offset
+    gk.ralign = r16, gk.calign = 1;
+    gk.RB = (M + r16 - 1 + r16 - 1) / r16 * r16;  // covers M rows from an aligned start
+    ok = gk.RB * a.W <= 256;
+    if (ok) {
+      const uint64_t dims[2] = {(uint64_t)a.H * a.W, (uint64_t)a.N * a.C};
+      const uint64_t str[1] = {(uint64_t)a.H * a.W * es};
+      const uint32_t box[2] = {(uint32_t)(gk.RB * a.W), 64};
+      ok = make_map(&tm, cdt, 2, a.x, dims, str, box, false);
+      gk.box_bytes = (unsigned)(gk.RB * a.W * 64 * es);
+    }
+  } else {
+    ok = false;
   }
-  constexpr int TJB = k1_tjb(M);
-  dim3 grid((a.tw + TJB - 1) / TJB, a.N * a.th, a.Cp / 32);
-  input_transform_nchw<DT, M, M + 2, D><<<grid, 32 * TJB, 0, a.st>>>(
-      (const typename Tr::T*)a.x, a.C, a.H, a.W, a.pad, a.th, a.tw, a.Cp, *a.xp, (typename Tr::T*)a.V, a.qstride,
-      a.plane);
+  const int seg = (ok ? gk.TJB : 1) * M + 2;
+  if (ok) {
+    gk.slot_bytes = (gk.box_bytes + 127) / 128 * 128;
+    gk.SEGP = seg | 1;
+    // deepest raw ring / widest halo ring that keeps two CTAs per SM
+    const int cand[2][2] = {{3, NX + M}, {2, NX + M}};
+    size_t smem = 0;
+    for (int i = 0; i < 2; ++i) {
+      gk.NSLOT = cand[i][0], gk.RR = cand[i][1];
+      smem = 256 + (size_t)gk.NSLOT * gk.slot_bytes + (size_t)gk.RR * 32 * gk.SEGP * sizeof(PT);
+      if (smem <= 110 * 1024) break;
+    }
+    ok = smem <= 200 * 1024;
+    if (ok) {
+      auto kern = input_transform_tma<DT, M, NX, D>;
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int nthr = 32 * ((gk.TJB < 7 ? gk.TJB : 7) + K1_CONV_WARPS);   // compute + converter warps
+      dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
+      kern<<<grid, nthr, smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
+      return;
+    }
+  }
+  // fallback: synchronous staging (odd plane sizes, misaligned x)
+  int tjb = a.tw < 8 ? a.tw : 8;
+  while (tjb > 1 && (size_t)NX * (tjb * M + 2) * 256 > 64 * 1024) --tjb;
+  const size_t ring = (size_t)NX * (tjb * M + 2) * 256;
+  int vec = 1;
+  for (int b = 16; b >= 4; b /= 2)
+    if ((size_t)b >= es && a.W % (int)(b / es) == 0 && xa % b == 0) {
+      vec = (int)(b / es);
+      break;
+    }
+  auto kern = input_transform_pairs<DT, M, NX, D>;
+  if (ring > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
+  dim3 grid((a.tw + tjb - 1) / tjb, a.N * a.th, a.Cp / 64);
+  kern<<<grid, 32 * tjb, ring, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th, a.tw, a.Cp, tjb, vec, *a.xp,
+                                       (TT*)a.V, a.qstride, a.plane);
 }
 template <int DT, int M, int D>
 static void launch_out(const OutArgs& a) {
@@ -344,13 +773,13 @@ static void launch_out(const OutArgs& a) {
                                                           (typename Tr::T*)a.y);
 }
 
-// m in [2, 8], domain D in [m + 2, m + 6].
-#define WINO_ROW(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>, &F<DT, M, M + 5>, &F<DT, M, M + 6>}
+// m in [2, 8], domain D in [m + 2, m + 4] (at most two quadratic moduli).
+#define WINO_ROW(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>}
 #define WINO_TABLE(F, DT) \
   {WINO_ROW(F, DT, 2), WINO_ROW(F, DT, 3), WINO_ROW(F, DT, 4), WINO_ROW(F, DT, 5), WINO_ROW(F, DT, 6), WINO_ROW(F, DT, 7), WINO_ROW(F, DT, 8)}
 
 // per-dtype tables (xform_<dt>.cu)
-extern const InFn kInTableF32[7][5], kInTableF16[7][5], kInTableBF16[7][5];
-extern const OutFn kOutTableF32[7][5], kOutTableF16[7][5], kOutTableBF16[7][5];
+extern const InFn kInTableF32[7][3], kInTableF16[7][3], kInTableBF16[7][3];
+extern const OutFn kOutTableF32[7][3], kOutTableF16[7][3], kOutTableBF16[7][3];
 
 }  // namespace wino

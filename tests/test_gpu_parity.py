@@ -87,9 +87,14 @@ def test_weight_transform(dtype, name, lowering):
 @pytest.mark.parametrize("name,lowering,pad", [("lin4", "subsolver", 1), ("sup1_6", "subsolver", 1),
                                                ("lin3", "subsolver", 0), ("sup1_4", "residue", 1),
                                                ("lin8", "subsolver", 1)])
-def test_input_transform(dtype, name, lowering, pad):
+@pytest.mark.parametrize("shape", [(2, 40, 19, 23), (2, 40, 28, 28), (1, 72, 18, 32), (2, 8, 14, 14)],
+                         ids=["odd-sync", "w28-flat16-3d32", "w32-3d", "w14-flat"])
+def test_input_transform(dtype, name, lowering, pad, shape):
+    """K1 vs the oracle's pipeline-mode V (rd(B^T d B), Eq. 2) on shapes that
+    reach each staging path: odd planes (synchronous), W*es % 16 != 0 with whole
+    rows (TMA flat boxes), W*es % 16 == 0 (TMA 3D boxes), channels < 64."""
     a, ref, m = algo_pair(name, lowering)
-    N, C, H, Wd = 2, 40, 19, 23
+    N, C, H, Wd = shape
     x, _ = datagen.layer(N, C, 1, H, Wd, dtype, seed=4)
     V = W.wino_input_transform(dev(x, dtype), a, pad=pad)
     torch.cuda.synchronize()
