@@ -6,8 +6,9 @@ Winograd-domain GEMM, K4 output transform) over one batch of synthetic input.
 Default workload (BASELINE.json configs[4], the largest single-GPU config the
 metric is quoted on): N=256, C=K=512, 28x28, pad 1, post-ReLU inputs, He
 weights; F(4x4, 3x3) Toom-Cook {0,-1,1,-1/2,1/2,inf} in bf16.  Under torchrun
-the global batch is sharded over ranks (strong scaling); the only collective
-is the NCCL all-reduce of the error statistics, outside the timed region.
+every rank runs its own N=256 images (weak scaling: the layer partitions over
+the batch with no exchange step); the only collective is the
+NCCL all-reduce of the error statistics, outside the timed region.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--algo lin4] [--dtype bf16]
     python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
@@ -150,7 +151,7 @@ def run_reference(a, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
         "config": {"workload": c["desc"], "algo": f"{a.algo} {{{T.moduli_spec(mods)}}}", "sample": sample},
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -214,11 +215,12 @@ def main():
     spec, m = canonical_spec(a.algo)
     algo = Wn.WinoAlgo(spec, m, lowering=a.lowering)
     tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[a.dtype]
-    N = c["N"]
-    assert N % world == 0, "global batch must divide over ranks"
-    nl = N // world
-    x64, w64 = datagen.layer(N, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=0, xdist=c["xdist"])
-    x64 = x64[rank * nl:(rank + 1) * nl]
+    from paper_1905_05233_b200 import distributed as D
+    nl = c["N"]                     # images per rank (weak scaling)
+    N = nl * world                  # global batch
+    # rank r draws its own images (seed r); the weights are the seed-0 weights on every rank
+    x64, _ = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=rank, xdist=c["xdist"])
+    _, w64 = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=0, xdist=c["xdist"])
     x = torch.from_numpy(np.ascontiguousarray(x64)).to(tdt).cuda()
     w = torch.from_numpy(w64).to(tdt).cuda()
     del x64
@@ -249,18 +251,17 @@ def main():
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        ms = D.max_over_ranks(ms, dist, "cuda")
     flops = direct_flops(N, C, K, Ho, Wo)
     value = flops / (ms * 1e-3) / 1e12
 
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-           "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+           "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
            "config": {"workload": c["desc"], "algo": f"{a.algo} {{{spec}}} m={m} mu={algo.mu} ratio={algo.ratio_2d:.4g}",
-                      "lowering": a.lowering, "global_batch": N, "parallelism": f"dp{world} (batch-sharded)",
+                      "lowering": a.lowering, "global_batch": N, "per_gpu_batch": nl,
+                      "parallelism": f"dp{world} (batch-partitioned, no data-path collective)",
                       "l2": "inputs larger than L2 (x %.0f MB, V and M staged through HBM)" % (
                           x.numel() * x.element_size() / 1e6 * world)},
            "gpu_launches": launches, "clocks": clk.summary()}
@@ -280,13 +281,8 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
     yref = Wn.wino_direct_conv2d_f64(x, w, 1, stream=st)
     stats = Wn.wino_error_stats(y, yref, m, stream=st)
     if world > 1:
-        s_sum = stats.clone()
-        s_sum[4] = 0
-        dist.all_reduce(s_sum)
-        s_max = stats[4:5].clone()
-        dist.all_reduce(s_max, op=dist.ReduceOp.MAX)
-        s_sum[4] = s_max[0]
-        stats = s_sum
+        from paper_1905_05233_b200 import distributed as D
+        stats = D.reduce_stats(stats, dist)
     out["accuracy"] = {k: (float(v) if not isinstance(v, int) else v) for k, v in Wn.summary(stats.cpu()).items()}
     del yref
     # ---------------------------------------------------------------- per-kernel breakdown (same stream, events)
@@ -335,9 +331,10 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
                            "peak_source": peak_src}
     # ---------------------------------------------------------------- layer-level rooflines (north star)
     ms = out["ms_per_step"]
-    comp_bytes = (xb + yb) * world + wb
-    t_roof = max(gemm_flops * world / tc_peak, comp_bytes / hbm)
-    t_staged = max(gemm_flops * world / tc_peak, (comp_bytes + (Ub + 2 * Vb + 2 * Mb) * world) / hbm)
+    # per GPU (every rank runs the same per-GPU layer concurrently)
+    comp_bytes = xb + yb + wb
+    t_roof = max(gemm_flops / tc_peak, comp_bytes / hbm)
+    t_staged = max(gemm_flops / tc_peak, (comp_bytes + Ub + 2 * Vb + 2 * Mb) / hbm)
     out["layer_roofline"] = {"t_roof_us": t_roof * 1e6, "frac_compulsory": t_roof / (ms * 1e-3),
                              "t_staged_us": t_staged * 1e6, "frac_staged": t_staged / (ms * 1e-3),
                              "peaks": peak_src}
@@ -407,10 +404,9 @@ def e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist):
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+        from paper_1905_05233_b200 import distributed as D
+        ms = D.max_over_ranks(ms, dist, "cuda")
     N = nl * world
     return {"value": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": ms,
             "h2d_bytes_per_step": x.numel() * x.element_size() * world,

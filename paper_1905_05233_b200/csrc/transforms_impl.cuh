@@ -399,6 +399,9 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 }
 
 constexpr int K1_CONV_WARPS = 4;   // converter warps of input_transform_tma
+// compute warps per CTA: 7 for the fully unrolled small tiles, 5 for the rolled
+// larger ones (keeps two CTAs per SM with room for their registers)
+__host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_nchunk(NX, D) == 1 ? 7 : 5; }
 
 struct K1Geo {
   int C, H, W, pad, th, tw, Cp, TJB;
@@ -408,7 +411,7 @@ struct K1Geo {
 };
 
 template <int DT, int M, int NX, int D>
-__global__ void __launch_bounds__(352, 2) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), 2) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
                                                               const __grid_constant__ K1Geo gk,
                                                               const __grid_constant__ XformParams xp,
                                                               typename DType<DT>::T* __restrict__ V, size_t qstride,
@@ -743,7 +746,8 @@ static void launch_in(const InArgs& a) {
     if (ok) {
       auto kern = input_transform_tma<DT, M, NX, D>;
       if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      const int nthr = 32 * ((gk.TJB < 7 ? gk.TJB : 7) + K1_CONV_WARPS);   // compute + converter warps
+      constexpr int MAXCW = k1_maxcw(NX, D);
+      const int nthr = 32 * ((gk.TJB < MAXCW ? gk.TJB : MAXCW) + K1_CONV_WARPS);   // compute + converter warps
       dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
       kern<<<grid, nthr, smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
       return;
