@@ -224,6 +224,9 @@ LAYER_CASES = [
     ("sup1_4", "residue", 2, 72, 40, 19, 23, 1),
     ("sup1_6", "residue", 1, 128, 136, 30, 30, 1),
     ("sup2_4", "residue", 1, 64, 48, 20, 20, 1),
+    ("lin4", "subsolver", 1, 3, 64, 224, 224, 1),       # VGG conv1_1: C = 3, 224 wide (3D TMA boxes, column blocks)
+    ("lin4", "subsolver", 2, 128, 128, 14, 14, 1),      # VGG block 5 spatial size (flat boxes, 4-row alignment)
+    ("sup1_6", "subsolver", 1, 64, 72, 56, 56, 1),      # VGG block 3 spatial size, m = 6
 ]
 
 
@@ -376,3 +379,41 @@ def test_full_size_sampled(cfg, name, dtype):
     else:
         assert abs(ss["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (ss, so)
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.15, (sg, so)   # whole layer vs sample
+
+
+VGG16_STACK = [(3, 64), (64, 64), "pool", (64, 128), (128, 128), "pool", (128, 256), (256, 256), (256, 256), "pool",
+               (256, 512), (512, 512), (512, 512), "pool", (512, 512), (512, 512), (512, 512)]
+
+
+@pytest.mark.parametrize("name", ["lin4", "sup1_6"])
+def test_vgg16_stack_per_layer(name):
+    """BASELINE cfg4 in miniature: the 13 conv layers of VGG-16 (channel schedule
+    64..512, ReLU after every conv, 2x2 max-pool between blocks; DESIGN.md
+    reading A16) on a 1 x 3 x 48 x 48 U[0,1) image with He weights, bf16.  Each
+    layer runs on the GPU's own previous activation (chained), and its error is
+    compared with the oracle's pipeline emulation on the same input (+-10 %)."""
+    dtype = "bf16"
+    a, ref, m = algo_pair(name)
+    rng = np.random.default_rng(5)
+    x = datagen.to_dtype_values(rng.random((1, 3, 48, 48)), dtype)
+    act = dev(x, dtype)
+    li = 0
+    for layer in VGG16_STACK:
+        if layer == "pool":
+            act = torch.nn.functional.max_pool2d(act, 2)
+            continue
+        cin, cout = layer
+        w = datagen.to_dtype_values(rng.normal(0.0, datagen.he_sigma(cin), (cout, cin, 3, 3)), dtype)
+        xin = host(act)
+        y = W.wino_conv2d(act, dev(w, dtype), a)
+        torch.cuda.synchronize()
+        yg = host(y)
+        yref = CV.direct_conv2d_f64(xin, w, 1)
+        yo = P.pipeline_conv2d(ref, xin, w, dtype)
+        sg = MT.summary(MT.stats8(yg, yref, m))
+        so = MT.summary(MT.stats8(yo, yref, m))
+        assert sg["nonfinite"] == so["nonfinite"] == 0
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (li, cin, cout, sg, so)
+        act = torch.relu(y)
+        li += 1
+    assert li == 13
