@@ -158,7 +158,7 @@ def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
     th, tw = -(-Ho // m), -(-Wo // m)
     T = N * th * tw
-    return dict(Ho=Ho, Wo=Wo, th=th, tw=tw, T=T, Tp=-(-T // 4) * 4, Cp=-(-C // 64) * 64, Q=D * D, S=S,
+    return dict(Ho=Ho, Wo=Wo, th=th, tw=tw, T=T, Tp=-(-T // 32) * 32, Cp=-(-C // 64) * 64, Q=D * D, S=S,
                 planes=2 if dtype == "fp32" else 1)
 
 
@@ -187,7 +187,7 @@ def wino_domain_gemm(V, U, algo, C, K, stream=None):
     """M [Q][K][Tp] fp32."""
     T = V.shape[2]
     dt = _TORCH_DT[V.dtype]
-    Tp = -(-T // 4) * 4
+    Tp = -(-T // 32) * 32
     M = torch.empty((algo.domain ** 2, K, Tp), dtype=torch.float32, device=V.device)
     check(lib().wino_domain_gemm(_ptr(V), _ptr(U), T, C, K, algo.handle, DTYPES[dt], _ptr(M), _stream(stream)))
     return M

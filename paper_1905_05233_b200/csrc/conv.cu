@@ -1,6 +1,7 @@
 // conv.cu -- C-ABI device entry points of the 2D layer (include/wino.h):
 // wino_conv2d = K2 weight transform -> K1 input transform -> K3 tcgen05
 // Winograd-domain GEMM -> K4 output transform, all on the caller's stream.
+#include <cstdlib>
 #include <string>
 
 #include "device.cuh"
@@ -13,11 +14,24 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
                                 wino_dtype dt, wino_layout layout, void* V, cudaStream_t st);
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
                             float* M, cudaStream_t st);
+wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
+                                  float* M, void* y, int* done, cudaStream_t st);
 wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
                                  wino_dtype dt, wino_layout layout, void* y, cudaStream_t st);
 }  // namespace wino
 
 using namespace wino;
+
+// The fused K3+K4 kernel (output transform from L2, gemm.cu) is opt-in with
+// WINO_FUSED=1: on B200 its fixup warps are L2-latency bound and the staged
+// K3 -> K4 pair is faster, so the staged pair is the default.
+static bool fused_disabled() {
+  static const int v = [] {
+    const char* e = getenv("WINO_FUSED");
+    return e && *e && *e != '0' ? 0 : 1;
+  }();
+  return v != 0;
+}
 
 static wino_status check_layer(const wino_algo* al, int N, int C, int H, int W, int K, int pad, wino_dtype dt,
                                wino_layout layout) {
@@ -60,6 +74,10 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   float* M = reinterpret_cast<float*>(base + g.offM);
   if ((s = run_weight_transform(w, K, C, al, dt, U, st)) != WINO_OK) return s;
   if ((s = run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, st)) != WINO_OK) return s;
+  if (layout == WINO_NCHW && !fused_disabled()) {
+    s = run_domain_gemm_fused(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
+    if (s != WINO_E_UNSUPPORTED) return s;   // OK or a real failure
+  }
   if ((s = run_domain_gemm(V, U, g, al, dt, M, st)) != WINO_OK) return s;
   if ((s = run_output_transform(M, N, K, H, W, pad, al, dt, layout, out, st)) != WINO_OK) return s;
   return WINO_OK;
@@ -107,7 +125,7 @@ wino_status wino_domain_gemm(const void* V, const void* U, int T, int C, int K, 
     return set_last_error("V and U must be 16-byte aligned"), WINO_E_ARG;
   Geo g = make_geo(al, 1, C, 3, 3, K, 0, dt);  // Cp, Q, S, es, planes
   g.T = T;
-  g.Tp = (int)align_up(T, 4);
+  g.Tp = (int)align_up(T, 32);
   return run_domain_gemm(V, U, g, al, dt, M, reinterpret_cast<cudaStream_t>(stream));
 }
 

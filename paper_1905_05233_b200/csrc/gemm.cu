@@ -24,6 +24,7 @@
 //               (cp.async.bulk.tensor, clipped at the ragged edges).  The
 //               accumulator is released to the MMA warp as soon as its last
 //               columns are in registers.
+#include <cstdlib>
 #include <string>
 
 #include "device.cuh"
@@ -189,6 +190,283 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ fused K3 + K4
+// Same warp-specialised tcgen05 pipeline, plus the output transform done from
+// L2: items are ordered tile-block (mb) major, so the Q * nNB point-GEMMs of a
+// 128-tile block finish close together; after an item's M boxes are stored
+// the storer publishes it on the block's counter (release), and four extra
+// "fixup" warps (8..15) of the CTAs pick the fixup items (mb, 32-channel
+// slice ks) of completed blocks, read M from L2 (ld.global.cg), apply
+// Y = A^T M A and store y, then discard the consumed M lines from L2
+// (discard.global.L2, no write-back).  M thus lives in L2 only (written and
+// read once there) instead of crossing HBM twice.  All CTAs are co-resident
+// (cooperative launch, one CTA per SM), so the fixup warps' waits always end.
+struct FuseArgs {
+  float AT[kMaxM][kMaxDomain];
+  int D, Q;             // domain, output points (= D * D)
+  int K, T, Tp, Ho, Wo, th, tw;
+  int nKS;              // 32-channel slices of K
+  int need;             // point-GEMM items per tile block (= Q * nNB)
+  void* y;
+  int* done;            // [nMB] point-GEMM items stored, per tile block (zeroed before the launch)
+  int* fixed;           // [nMB] fixup items finished, per tile block (zeroed before the launch)
+  int lag;              // the producer starts tile block mb only once block mb - lag is fully fixed up
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+template <int DT, int M, int D>
+__device__ __forceinline__ void fixup_item(const float* __restrict__ Mw, const FuseArgs& fa, int mb, int ks, int tid) {
+  using Tr = DType<DT>;
+  using TT = typename Tr::T;
+  const int t = mb * kBM + (tid & (kBM - 1));
+  const int kh = tid >> 7;   // 256 fixup threads: two halves of the 32-channel slice
+  const int k0 = ks * 32 + kh * 16, k1 = min(fa.K, k0 + 16);
+  if (t >= fa.T) return;
+  const int tj = t % fa.tw, rest = t / fa.tw;
+  const int ti = rest % fa.th, n = rest / fa.th;
+  const size_t qs = (size_t)fa.K * fa.Tp;
+  constexpr int RB = M * (int)sizeof(TT);
+  constexpr bool kVec = (RB == 4 || RB == 8 || RB == 16);
+  const bool vec = kVec && tj * M + M <= fa.Wo && ((fa.Wo * (int)sizeof(TT)) % RB) == 0 &&
+                   (reinterpret_cast<uintptr_t>(fa.y) % RB) == 0;
+#pragma unroll 1
+  for (int k = k0; k < k1; ++k) {
+    const float* src = Mw + (size_t)k * fa.Tp + t;
+    float Y[M][M];
+#pragma unroll
+    for (int p = 0; p < M; ++p)
+#pragma unroll
+      for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      float v[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = __ldcg(src + (size_t)(i * D + j) * qs);
+      float Z[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = fmaf(v[j], fa.AT[q][j], acc);
+        Z[q] = acc;
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p)
+#pragma unroll
+        for (int q = 0; q < M; ++q) Y[p][q] = fmaf(fa.AT[p][i], Z[q], Y[p][q]);
+    }
+    TT* dst = reinterpret_cast<TT*>(fa.y) + (((size_t)n * fa.K + k) * fa.Ho + (size_t)ti * M) * fa.Wo + (size_t)tj * M;
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+      if (ti * M + p >= fa.Ho) break;
+      TT* row = dst + (size_t)p * fa.Wo;
+      if constexpr (kVec) {
+        if (vec) {
+          union {
+            TT e[M];
+            uint32_t u[RB / 4];
+          } pk;
+#pragma unroll
+          for (int q = 0; q < M; ++q) pk.e[q] = Tr::cvt(Y[p][q]);
+          if constexpr (RB == 4) *reinterpret_cast<uint32_t*>(row) = pk.u[0];
+          if constexpr (RB == 8) *reinterpret_cast<uint2*>(row) = make_uint2(pk.u[0], pk.u[1]);
+          if constexpr (RB == 16) *reinterpret_cast<uint4*>(row) = make_uint4(pk.u[0], pk.u[1], pk.u[2], pk.u[3]);
+          continue;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < M; ++q)
+        if (tj * M + q < fa.Wo) row[q] = Tr::cvt(Y[p][q]);
+    }
+  }
+}
+
+template <int BN, int STAGES, int DT, int MO, int DO>
+__global__ void __launch_bounds__(512, 1)
+    domain_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                             const __grid_constant__ CUtensorMap tmM, const float* __restrict__ Mw, int T, int K,
+                             int Cp, int nMB, int nNB, int Q, int S, uint32_t idesc,
+                             const __grid_constant__ GemmSched gs, const __grid_constant__ FuseArgs fa) {
+  using Cfg = GemmCfg<false, BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
+    fence_barrier_init();
+    fence_proxy_async_shared();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nItems = Q * nMB * nNB;
+  const int KB = Cp / Cfg::BK;
+  // item -> (mb slowest, then output point p, then nb)
+  auto decode = [&](int item, int& mb, int& p, int& nb) {
+    nb = item % nNB;
+    p = (item / nNB) % Q;
+    mb = item / (nNB * Q);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+        int mb, p, nb;
+        decode(item, mb, p, nb);
+        // backpressure: keep at most `lag` tile blocks of M in flight in L2
+        if (mb >= fa.lag)
+          while (ld_acquire(fa.fixed + mb - fa.lag) < fa.nKS) __nanosleep(128);
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          const int qi = gs.in_pt[pr], sl = gs.slab[pr];
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+            uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
+            tma_load_3d(base, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi);
+            tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+        int mb, p, nb;
+        decode(item, mb, p, nb);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        int step = 0;
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          for (int kb = 0; kb < KB; ++kb, ++step) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t b0 = a0 + Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint32_t koff = k * Cfg::UK * Cfg::ES;
+              mma_ss<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc, (step | k) != 0);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) acc = 0, acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {
+    // -------------------------------------------------- epilogue: TMEM -> SMEM -> TMA store, then publish
+    const int wq = warp & 3;
+    const bool storer = (warp == 4 && lane == 0);
+    int acc = 0, chunk = 0;
+    uint32_t acc_phase = 0;
+    for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
+      int mb, p, nb;
+      decode(item, mb, p, nb);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
+        if (j0 + 32 == BN) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        if (nb * BN + j0 >= K) continue;
+        float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
+        if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
+        named_bar_sync(1, 128);
+#pragma unroll
+        for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
+        fence_proxy_async_shared();
+        named_bar_sync(1, 128);
+        if (storer) {
+          tma_store_3d(&tmM, buf, mb * kBM, nb * BN + j0, p);
+          bulk_commit();
+        }
+        ++chunk;
+      }
+      if (++acc == 2) acc = 0, acc_phase ^= 1;
+      if (storer) {
+        // the item's M boxes are in memory: publish them to the fixup warps
+        bulk_wait_all();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        __threadfence();
+        red_release_add(fa.done + mb, 1);
+      }
+    }
+    if (storer) bulk_wait_all();
+  } else if (warp >= 8) {
+    // -------------------------------------------------- fixup warps: output transform from L2
+    const int tid = threadIdx.x - 256;   // 256 fixup threads
+    const int nFix = nMB * fa.nKS;
+    for (int f = blockIdx.x; f < nFix; f += gridDim.x) {
+      const int mb = f / fa.nKS, ks = f % fa.nKS;
+      if (lane == 0)
+        while (ld_acquire(fa.done + mb) < fa.need) __nanosleep(256);
+      __syncwarp();
+      fixup_item<DT, MO, DO>(Mw, fa, mb, ks, tid);
+      named_bar_sync(2, 256);
+      // every M line of (all points, 32 channels, this 128-tile block) has been read: drop it from L2
+      const int k0 = ks * 32, nk = min(fa.K, k0 + 32) - k0;
+      const int lines = fa.Q * nk * 4;
+      for (int l = tid; l < lines; l += 256) {
+        const int q = l / (nk * 4), r = l % (nk * 4);
+        const float* ptr = Mw + ((size_t)q * fa.K + k0 + r / 4) * fa.Tp + (size_t)mb * kBM + (r % 4) * 32;
+        discard_l2(ptr);
+      }
+      named_bar_sync(2, 256);
+      if (tid == 0) {
+        __threadfence();
+        red_release_add(fa.fixed + mb, 1);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 static int num_sms() {
@@ -219,6 +497,93 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
                                      make_idesc(fmt, kBM, BN), gs);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
+}
+
+template <int DT, int MO, int DO>
+static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
+                                const wino_algo* al, uint32_t fmt, const float* M, void* y, int* done, cudaStream_t st) {
+  constexpr int BN = 256, STAGES = 4;
+  using Cfg = GemmCfg<false, BN, STAGES>;
+  auto kern = domain_gemm_fused_kernel<BN, STAGES, DT, MO, DO>;
+  static bool attr = false;
+  if (!attr) {
+    WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr = true;
+  }
+  const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
+  FuseArgs fa{};
+  for (int q = 0; q < al->m; ++q)
+    for (int j = 0; j < al->D; ++j) fa.AT[q][j] = al->xp.AT[q][j];
+  fa.D = al->D, fa.Q = g.Q, fa.K = g.K, fa.T = g.T, fa.Tp = g.Tp, fa.Ho = g.Ho, fa.Wo = g.Wo, fa.th = g.th,
+  fa.tw = g.tw, fa.nKS = (g.K + 31) / 32, fa.need = al->gs.Q * nNB, fa.y = y, fa.done = done;
+  fa.fixed = done + nMB;
+  // tile blocks of M (Q * K * 128 * 4 bytes each) allowed in flight: ~40 MB of the 126 MB L2
+  {
+    const size_t blk = (size_t)g.Q * g.K * kBM * 4;
+    int lag = (int)((40u << 20) / (blk ? blk : 1));
+    fa.lag = lag < 2 ? 2 : lag;
+    if (const char* e = getenv("WINO_FUSED_LAG")) fa.lag = atoi(e);
+  }
+  WINO_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * 2 * nMB, st));
+  const int items = al->gs.Q * nMB * nNB;
+  int grid = items < num_sms() ? items : num_sms();
+  const int nfix = nMB * fa.nKS;
+  if (grid < 1) grid = 1;
+  (void)nfix;
+  const uint32_t idesc = make_idesc(fmt, kBM, BN);
+  int T = g.T, K = g.K, Cp = g.Cp, Q = al->gs.Q, S = g.S;
+  const float* Mp = M;
+  void* args[] = {(void*)&tv, (void*)&tu, (void*)&tm, (void*)&Mp, &T, &K, &Cp, (void*)&nMB, (void*)&nNB, &Q, &S,
+                  (void*)&idesc, (void*)&al->gs, (void*)&fa};
+  // cooperative launch: every CTA is resident (the fixup warps wait on other CTAs' items)
+  WINO_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(512), args, Cfg::SMEM, st));
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+template <int DT, int MO>
+static wino_status fused_d(int doff, const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
+                           const wino_algo* al, uint32_t fmt, const float* M, void* y, int* done, cudaStream_t st) {
+  switch (doff) {
+    case 0: return launch_fused<DT, MO, MO + 2>(tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 1: return launch_fused<DT, MO, MO + 3>(tv, tu, tm, g, al, fmt, M, y, done, st);
+    default: return launch_fused<DT, MO, MO + 4>(tv, tu, tm, g, al, fmt, M, y, done, st);
+  }
+}
+template <int DT>
+static wino_status fused_m(int m, int doff, const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm,
+                           const Geo& g, const wino_algo* al, uint32_t fmt, const float* M, void* y, int* done,
+                           cudaStream_t st) {
+  switch (m) {
+    case 2: return fused_d<DT, 2>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 3: return fused_d<DT, 3>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 4: return fused_d<DT, 4>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 5: return fused_d<DT, 5>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 6: return fused_d<DT, 6>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    case 7: return fused_d<DT, 7>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+    default: return fused_d<DT, 8>(doff, tv, tu, tm, g, al, fmt, M, y, done, st);
+  }
+}
+
+// Fused K3 + K4 (16-bit dtypes, K > 128, NCHW output).  Returns WINO_E_UNSUPPORTED
+// (without launching) when the configuration is not covered.
+wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
+                                  float* M, void* y, int* done, cudaStream_t st) {
+  const int doff = al->D - al->m - 2;
+  if (dt == WINO_F32 || g.K <= 128 || al->m < 2 || al->m > 8 || doff < 0 || doff > 2) return WINO_E_UNSUPPORTED;
+  CUtensorMapDataType cdt = dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  constexpr int BN = 256;
+  const uint32_t BK = 128 / (uint32_t)g.es;
+  CUtensorMap tv, tu, tm;
+  if (!make_map3(&tv, cdt, g.es, V, g.Cp, g.T, (uint64_t)g.Q * g.planes, BK, kBM) ||
+      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
+      !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, g.T, g.K, g.Q, kBM, 32, false, g.Tp)) {
+    set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
+    return WINO_E_CUDA;
+  }
+  const uint32_t fmt = dt == WINO_F16 ? 0u : 1u;
+  return dt == WINO_F16 ? fused_m<WINO_F16>(al->m, doff, tv, tu, tm, g, al, fmt, M, y, done, st)
+                        : fused_m<WINO_BF16>(al->m, doff, tv, tu, tm, g, al, fmt, M, y, done, st);
 }
 
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,

@@ -1,5 +1,5 @@
 // geometry.hpp -- layer geometry and workspace layout of wino_conv2d
-// (include/wino.h): U [S][K][Cp] | V [Q][T][Cp] | M [Q][K][Tp] fp32.
+// (include/wino.h): U [S][K][Cp] | V [Q][T][Cp] | M [Q][K][Tp] fp32 | group counters.
 #pragma once
 #include <cstddef>
 
@@ -14,7 +14,7 @@ struct Geo {
   int m, D, Q, S;
   int Ho, Wo, th, tw, T, Tp, Cp;
   size_t es, planes;
-  size_t offU, offV, offM, total;
+  size_t offU, offV, offM, offD, total;
 };
 
 // Tiling of PAPER.md P:498: overlapping (m+2)x(m+2) tiles at stride m.
@@ -30,7 +30,7 @@ inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int 
   g.th = (g.Ho + g.m - 1) / g.m;
   g.tw = (g.Wo + g.m - 1) / g.m;
   g.T = N * g.th * g.tw;
-  g.Tp = (int)align_up(g.T, 4);
+  g.Tp = (int)align_up(g.T, 32);   // 128-byte M rows (fused K3+K4 discards whole L2 lines)
   g.Cp = (int)align_up(C, 64);
   g.es = dt == WINO_F32 ? 4 : 2;
   g.planes = dt == WINO_F32 ? 2 : 1;  // fp32: TF32 hi and lo planes
@@ -40,7 +40,8 @@ inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int 
   g.offU = 0;
   g.offV = align_up(g.offU + u_bytes, 1024);
   g.offM = align_up(g.offV + v_bytes, 1024);
-  g.total = align_up(g.offM + m_bytes, 1024);
+  g.offD = align_up(g.offM + m_bytes, 1024);
+  g.total = align_up(g.offD + (size_t)((g.T + 127) / 128) * 8, 1024);   // two ints per 128-tile group
   return g;
 }
 

@@ -176,7 +176,7 @@ def test_output_transform(dtype, name, lowering):
     rng = np.random.default_rng(8)
     D = a.domain
     Mh = rng.standard_normal((D * D, K, T_)).astype(np.float32)
-    Md = torch.zeros((D * D, K, -(-T_ // 4) * 4), dtype=torch.float32)
+    Md = torch.zeros((D * D, K, -(-T_ // 32) * 32), dtype=torch.float32)   # Tp: T rounded up to 32
     Md[:, :, :T_] = torch.from_numpy(Mh)
     y = W.wino_output_transform(Md.cuda(), a, N, K, H, Wd, 1, dtype)
     torch.cuda.synchronize()
@@ -194,7 +194,7 @@ def _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad, xdist="relu_normal"
     a, ref, m = algo_pair(name, lowering)
     x, w = datagen.layer(N, C, K, H, Wd, dtype, seed=seed, xdist=xdist)
     y = W.wino_conv2d(dev(x, dtype), dev(w, dtype), a, pad=pad)
-    assert W.wino_last_launch_count() == 4
+    assert W.wino_last_launch_count() in (3, 4)   # K2, K1, fused K3+K4 | K3, K4
     torch.cuda.synchronize()
     yg = host(y)
     yref = CV.direct_conv2d_f64(x, w, pad)
@@ -417,3 +417,40 @@ def test_vgg16_stack_per_layer(name):
         act = torch.relu(y)
         li += 1
     assert li == 13
+
+
+def test_fused_gemm_output_transform_matches_staged():
+    """The opt-in fused K3+K4 kernel (WINO_FUSED=1, output transform from L2) gives
+    bit-identical y to the staged K3 -> K4 pair (same fp32 arithmetic per
+    output; only where M lives differs).  Runs in a subprocess because the
+    switch is read once per process."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, '.')
+import datagen, paper_1905_05233_b200 as W
+from paper_1905_05233_b200.algos import canonical_spec
+out = []
+for name, dt in (('lin4', 'bf16'), ('sup1_6', 'fp16')):
+    spec, m = canonical_spec(name)
+    a = W.WinoAlgo(spec, m)
+    x, w = datagen.layer(3, 96, 272, 23, 19, dt, seed=2)
+    td = {'bf16': torch.bfloat16, 'fp16': torch.float16}[dt]
+    y = W.wino_conv2d(torch.from_numpy(x).to(td).cuda(), torch.from_numpy(w).to(td).cuda(), a)
+    torch.cuda.synchronize()
+    out.append(y.float().cpu().numpy())
+np.save(sys.argv[1], np.concatenate([o.ravel() for o in out]))
+"""
+    import os
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for fused in ("0", "1"):
+        f = tempfile.NamedTemporaryFile(suffix=".npy", delete=False).name
+        env = dict(os.environ, WINO_FUSED=fused)
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
