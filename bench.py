@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--algo", default="lin4")
     ap.add_argument("--dtype", default="bf16", choices=["fp32", "fp16", "bf16"])
     ap.add_argument("--lowering", default="subsolver", choices=["subsolver", "residue"])
+    ap.add_argument("--layout", default="nchw", choices=["nchw", "nhwc"],
+                    help="activation layout of x and y (BASELINE's x[N,C,H,W] is nchw)")
     ap.add_argument("--sweep", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--no-extras", action="store_true", help="timed loop only (for ncu launch lists)")
     return ap.parse_args()
@@ -222,16 +224,18 @@ def main():
     x64, _ = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=rank, xdist=c["xdist"])
     _, w64 = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=0, xdist=c["xdist"])
     x = torch.from_numpy(np.ascontiguousarray(x64)).to(tdt).cuda()
+    if a.layout == "nhwc":
+        x = x.permute(0, 2, 3, 1).contiguous()
     w = torch.from_numpy(w64).to(tdt).cuda()
     del x64
     C, K, H, W = c["C"], c["K"], c["H"], c["W"]
     Ho, Wo = H, W
-    y = torch.empty((nl, K, Ho, Wo), dtype=tdt, device="cuda")
-    ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, nl, C, H, W, K, 1, a.dtype))
+    y = torch.empty((nl, K, Ho, Wo) if a.layout == "nchw" else (nl, Ho, Wo, K), dtype=tdt, device="cuda")
+    ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, nl, C, H, W, K, 1, a.dtype, a.layout))
     st = torch.cuda.current_stream()
 
     def step():
-        Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st)
+        Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st, layout=a.layout)
         return Wn.wino_last_launch_count()
 
     for _ in range(max(3, a.warmup)):
@@ -260,7 +264,7 @@ def main():
            "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
            "config": {"workload": c["desc"], "algo": f"{a.algo} {{{spec}}} m={m} mu={algo.mu} ratio={algo.ratio_2d:.4g}",
-                      "lowering": a.lowering, "global_batch": N, "per_gpu_batch": nl,
+                      "lowering": a.lowering, "layout": a.layout, "global_batch": N, "per_gpu_batch": nl,
                       "parallelism": f"dp{world} (batch-partitioned, no data-path collective)",
                       "l2": "inputs larger than L2 (x %.0f MB, V and M staged through HBM)" % (
                           x.numel() * x.element_size() / 1e6 * world)},
@@ -278,8 +282,11 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
     import paper_1905_05233_b200 as Wn
     peaks, peak_src = load_peaks()
     # ---------------------------------------------------------------- accuracy vs fp64 direct (device)
-    yref = Wn.wino_direct_conv2d_f64(x, w, 1, stream=st)
-    stats = Wn.wino_error_stats(y, yref, m, stream=st)
+    xc = x if a.layout == "nchw" else x.permute(0, 3, 1, 2).contiguous()
+    yc = y if a.layout == "nchw" else y.permute(0, 3, 1, 2).contiguous()
+    yref = Wn.wino_direct_conv2d_f64(xc, w, 1, stream=st)
+    stats = Wn.wino_error_stats(yc, yref, m, stream=st)
+    del xc, yc
     if world > 1:
         from paper_1905_05233_b200 import distributed as D
         stats = D.reduce_stats(stats, dist)
@@ -291,7 +298,8 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
     pl = g["planes"]
     U = ws[:0]
     base = ws.data_ptr()
-    kern = per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, a.dtype, max(20, a.steps // 4))
+    kern = per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, a.dtype, max(20, a.steps // 4),
+                            lay=0 if a.layout == "nchw" else 1)
     T_, Q, S, Cp, Tp = g["T"], g["Q"], g["S"], g["Cp"], g["Tp"]
     xb = x.numel() * x.element_size()
     yb = y.numel() * y.element_size()
@@ -347,7 +355,7 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
         out["sweep"] = sweep(c, st)
 
 
-def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps):
+def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps, lay=0):
     import torch
     import paper_1905_05233_b200 as Wn
     from paper_1905_05233_b200._lib import lib, check, DTYPES
@@ -366,10 +374,10 @@ def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps):
         "weight_transform": lambda: L.wino_weight_transform(ctypes.c_void_p(w.data_ptr()), K, C, algo.handle, d,
                                                             ctypes.c_void_p(U), s),
         "input_transform": lambda: L.wino_input_transform(ctypes.c_void_p(x.data_ptr()), nl, C, H, W, 1,
-                                                          algo.handle, d, 0, ctypes.c_void_p(V), s),
+                                                          algo.handle, d, lay, ctypes.c_void_p(V), s),
         "domain_gemm": lambda: L.wino_domain_gemm(ctypes.c_void_p(V), ctypes.c_void_p(U), g["T"], C, K,
                                                   algo.handle, d, ctypes.c_void_p(M), s),
-        "output_transform": lambda: L.wino_output_transform(ctypes.c_void_p(M), nl, K, H, W, 1, algo.handle, d, 0,
+        "output_transform": lambda: L.wino_output_transform(ctypes.c_void_p(M), nl, K, H, W, 1, algo.handle, d, lay,
                                                             ctypes.c_void_p(y.data_ptr()), s),
     }
     names = list(calls)
@@ -395,12 +403,12 @@ def e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist):
     yh = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
     steps = max(5, min(a.steps, 30))
     for _ in range(2):
-        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st)
+        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for _ in range(steps):
-        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st)
+        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
     e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps

@@ -123,16 +123,22 @@ def alloc_workspace(nbytes, device="cuda"):
 
 def wino_conv2d(x, w, algo, pad=1, layout="nchw", out=None, workspace=None, stream=None):
     """y = conv(x, w) (valid cross-correlation, stride 1, zero padding `pad`)
-    through libwino's kernels.  x: [N,C,H,W], w: [K,C,3,3], same dtype, CUDA."""
-    assert layout == "nchw"
-    N, C, H, W = x.shape
+    through libwino's kernels.  x: [N,C,H,W] ("nchw") or [N,H,W,C] ("nhwc"),
+    w: [K,C,3,3], same dtype, CUDA; y in the layout of x."""
+    if layout == "nchw":
+        N, C, H, W = x.shape
+    elif layout == "nhwc":
+        N, H, W, C = x.shape
+    else:
+        raise WinoError(1, f"bad layout {layout!r}")
     K = w.shape[0]
     assert w.shape == (K, C, 3, 3) and w.dtype == x.dtype and x.is_cuda and w.is_cuda
     x = x.contiguous()
     w = w.contiguous()
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
     if out is None:
-        out = torch.empty((N, K, Ho, Wo), dtype=x.dtype, device=x.device)
+        shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
+        out = torch.empty(shape, dtype=x.dtype, device=x.device)
     dt = _TORCH_DT[x.dtype]
     nbytes = wino_conv2d_workspace(algo, N, C, H, W, K, pad, dt, layout)
     if workspace is None:
@@ -142,13 +148,16 @@ def wino_conv2d(x, w, algo, pad=1, layout="nchw", out=None, workspace=None, stre
     return out
 
 
-def wino_conv2d_host_io(x_host, x_dev, w, algo, out_dev, out_host, workspace, pad=1, stream=None):
+def wino_conv2d_host_io(x_host, x_dev, w, algo, out_dev, out_host, workspace, pad=1, stream=None, layout="nchw"):
     """End-to-end call: pinned host x -> device -> layer -> pinned host y, on `stream`."""
-    N, C, H, W = x_dev.shape
+    if layout == "nchw":
+        N, C, H, W = x_dev.shape
+    else:
+        N, H, W, C = x_dev.shape
     K = w.shape[0]
     dt = _TORCH_DT[x_dev.dtype]
     check(lib().wino_conv2d_host_io(_ptr(x_host), _ptr(x_dev), _ptr(w), N, C, H, W, K, pad, algo.handle,
-                                    DTYPES[dt], 0, _ptr(out_dev), _ptr(out_host), _ptr(workspace),
+                                    DTYPES[dt], LAYOUTS[layout], _ptr(out_dev), _ptr(out_host), _ptr(workspace),
                                     workspace.numel(), _stream(stream)))
 
 
@@ -172,14 +181,17 @@ def wino_weight_transform(w, algo, stream=None):
     return U
 
 
-def wino_input_transform(x, algo, pad=1, stream=None):
-    """V [planes][Q][T][Cp] in the storage dtype."""
-    N, C, H, W = x.shape
+def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
+    """V [planes][Q][T][Cp] in the storage dtype; x [N,C,H,W] or [N,H,W,C] ("nhwc")."""
+    if layout == "nchw":
+        N, C, H, W = x.shape
+    else:
+        N, H, W, C = x.shape
     dt = _TORCH_DT[x.dtype]
     g = geometry(algo, N, C, H, W, 1, pad, dt)
     V = torch.empty((g["planes"], g["Q"], g["T"], g["Cp"]), dtype=x.dtype, device=x.device)
-    check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], 0, _ptr(V),
-                                     _stream(stream)))
+    check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
+                                     _ptr(V), _stream(stream)))
     return V
 
 
@@ -193,11 +205,12 @@ def wino_domain_gemm(V, U, algo, C, K, stream=None):
     return M
 
 
-def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None):
+def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None, layout="nchw"):
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
-    y = torch.empty((N, K, Ho, Wo), dtype=TORCH_OF[dtype], device=M.device)
-    check(lib().wino_output_transform(_ptr(M), N, K, H, W, pad, algo.handle, DTYPES[dtype], 0, _ptr(y),
-                                      _stream(stream)))
+    shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
+    y = torch.empty(shape, dtype=TORCH_OF[dtype], device=M.device)
+    check(lib().wino_output_transform(_ptr(M), N, K, H, W, pad, algo.handle, DTYPES[dtype], LAYOUTS[layout],
+                                      _ptr(y), _stream(stream)))
     return y
 
 

@@ -40,7 +40,6 @@ static wino_status check_layer(const wino_algo* al, int N, int C, int H, int W, 
     return set_last_error("bad layer geometry (need N, C, K > 0, pad in {0,1}, H, W + 2 pad >= 3)"), WINO_E_ARG;
   if (dt != WINO_F32 && dt != WINO_F16 && dt != WINO_BF16) return set_last_error("bad dtype"), WINO_E_ARG;
   if (layout != WINO_NCHW && layout != WINO_NHWC) return set_last_error("bad layout"), WINO_E_ARG;
-  if (layout != WINO_NCHW) return set_last_error("NHWC layout not implemented yet"), WINO_E_UNSUPPORTED;
   if (al->r != 3) return set_last_error("r != 3"), WINO_E_UNSUPPORTED;
   if (K > 65535) return set_last_error("K > 65535 unsupported"), WINO_E_UNSUPPORTED;
   return WINO_OK;

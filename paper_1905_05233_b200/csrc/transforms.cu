@@ -81,12 +81,13 @@ wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* a
 
 wino_status run_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
                                 wino_dtype dt, wino_layout layout, void* V, cudaStream_t st) {
-  if (layout != WINO_NCHW || !md_ok(al)) {
+  if ((layout != WINO_NCHW && layout != WINO_NHWC) || !md_ok(al)) {
     set_last_error("input transform: unsupported layout / (m, domain)");
     return WINO_E_UNSUPPORTED;
   }
   Geo g = make_geo(al, N, C, H, W, 1, pad, dt);
-  InArgs a{x, C, H, W, pad, g.th, g.tw, g.Cp, N, &al->xp, V, (size_t)g.T * g.Cp, (size_t)g.Q * g.T * g.Cp, st};
+  InArgs a{x, C, H, W, pad, g.th, g.tw, g.Cp, N, (int)layout, &al->xp, V, (size_t)g.T * g.Cp,
+           (size_t)g.Q * g.T * g.Cp, st};
   in_fn_(dt, al->m, al->D - al->m - 2)(a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
@@ -94,12 +95,12 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
 
 wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
                                  wino_dtype dt, wino_layout layout, void* y, cudaStream_t st) {
-  if (layout != WINO_NCHW || !md_ok(al)) {
+  if ((layout != WINO_NCHW && layout != WINO_NHWC) || !md_ok(al)) {
     set_last_error("output transform: unsupported layout / (m, domain)");
     return WINO_E_UNSUPPORTED;
   }
   Geo g = make_geo(al, N, 1, H, W, K, pad, dt);
-  OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, g.Tp, &al->xp, y, st};
+  OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, g.Tp, (int)layout, &al->xp, y, st};
   out_fn_(dt, al->m, al->D - al->m - 2)(a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;

@@ -558,6 +558,198 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), 2) inp
 #undef K1_ISSUE
 }
 
+// ------------------------------------------------------------------ K1 input transform (NHWC)
+// x[N][H][W][C]: channels are contiguous, so a TMA box {64 channels, BOXW
+// columns, NX rows} of the [N][H][W][C] tensor lands in shared memory as
+// [row][col][channel] -- already lane = channel pair (4-byte bf16x2 / half2,
+// 8-byte float2 words, consecutive lanes consecutive words: conflict-free).
+// No transpose: CTA = (tile-column block of TJB tiles, image, 64-channel
+// block) walks down the tile rows with an NSLOT-deep TMA ring (mbarriers),
+// each warp transforms one tile of the row from the box.  Boxes start at
+// non-negative coordinates (rows / columns before the image are predicated
+// to zero); TMA zero-fills beyond W, H and C.
+struct K1NGeo {
+  int C, H, W, pad, th, tw, Cp, TJB, BOXW, NSLOT;
+  unsigned box_bytes, slot_bytes;
+};
+
+template <int DT, int NX, int D, typename PT>
+__device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int rowoff, int colbase,
+                                                   const XformParams& xp, typename DType<DT>::T* out,
+                                                   size_t qstride, size_t plane) {
+  // element (a, q) of the tile: box row a + rowoff, column colbase + q (word
+  // index (row * BOXW + col) * 32 + lane, `box` already offset by lane);
+  // negative rows / columns are the zero padding
+  using P = PairT<DT>;
+  constexpr int JC = k1_jc(NX, D);
+  auto load_row = [&](int a, float2* d) {
+    const int r = a + rowoff;
+    const PT* sd = box + (size_t)(r < 0 ? 0 : r) * BOXW * 32;
+#pragma unroll
+    for (int q = 0; q < NX; ++q) {
+      const int c = colbase + q;
+      const float2 v = P::unpack(sd[(c < 0 ? 0 : c) * 32]);
+      d[q] = (r < 0 || c < 0) ? make_float2(0.f, 0.f) : v;
+    }
+  };
+  if constexpr (k1_nchunk(NX, D) == 1) {
+    float2 acc[D][D];
+#pragma unroll
+    for (int a = 0; a < NX; ++a) {
+      float2 d[NX];
+      load_row(a, d);
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+          const float c = xp.BT[j][q];
+          rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+        }
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          const float c = xp.BT[i][a];
+          acc[i][j] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
+  } else {
+#pragma unroll 1
+    for (int j0 = 0; j0 < D; j0 += JC) {
+      float2 acc[D][JC];
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) acc[i][jj] = make_float2(0.f, 0.f);
+#pragma unroll 1
+      for (int a = 0; a < NX; ++a) {
+        float2 d[NX];
+        load_row(a, d);
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj) {
+          float2 rt = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < NX; ++q) {
+            const float c = xp.BT[j0 + jj < D ? j0 + jj : D - 1][q];
+            rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+          }
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            const float c = xp.BT[i][a];
+            acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int jj = 0; jj < JC; ++jj)
+          if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+    }
+  }
+}
+
+template <int DT, int M, int NX, int D>
+__global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_constant__ CUtensorMap tmx,
+                                                               const __grid_constant__ K1NGeo gk,
+                                                               const __grid_constant__ XformParams xp,
+                                                               typename DType<DT>::T* __restrict__ V, size_t qstride,
+                                                               size_t plane) {
+  using PT = typename PairT<DT>::T;
+  extern __shared__ __align__(16) uint8_t kn_smem_raw[];
+  uint8_t* sm = kn_smem_raw + ((128u - (smem_u32(kn_smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint8_t* slots = sm + 128;
+  const int NSLOT = gk.NSLOT, th = gk.th, pad = gk.pad;
+  const int tj0 = blockIdx.x * gk.TJB, n = blockIdx.y, c0 = blockIdx.z * 64;
+  const int col0 = tj0 * M - pad, cst = col0 < 0 ? 0 : col0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1);
+    fence_barrier_init();
+    tma_prefetch(&tmx);
+  }
+  __syncthreads();
+#define KN_ISSUE(ti_)                                                                                        \
+  do {                                                                                                       \
+    const int s_ = (ti_) % NSLOT;                                                                            \
+    const int g_ = (ti_) * M - pad;                                                                          \
+    fence_proxy_async_shared();                                                                              \
+    mbar_arrive_expect_tx(&full[s_], gk.box_bytes);                                                          \
+    tma_load_4d(slots + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], c0, cst, g_ < 0 ? 0 : g_, n);           \
+  } while (0)
+  if (threadIdx.x == 0)
+    for (int ti = 0; ti < NSLOT && ti < th; ++ti) KN_ISSUE(ti);
+  const int ca = c0 + 2 * lane;
+#pragma unroll 1
+  for (int ti = 0; ti < th; ++ti) {
+    mbar_wait(&full[ti % NSLOT], (uint32_t)((ti / NSLOT) & 1));
+    const PT* box = reinterpret_cast<const PT*>(slots + (size_t)(ti % NSLOT) * gk.slot_bytes) + lane;
+    const int g = ti * M - pad;
+    const int rowoff = g - (g < 0 ? 0 : g);   // -pad for the first tile row, else 0
+    for (int tjl = warp; tjl < gk.TJB; tjl += nw) {
+      const int tj = tj0 + tjl;
+      if (tj >= gk.tw) break;
+      const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
+      transform_tile_box<DT, NX, D, PT>(box, gk.BOXW, rowoff, tjl * M + col0 - cst, xp, V + t * gk.Cp + ca, qstride,
+                                        plane);
+    }
+    __syncthreads();   // slot ti % NSLOT is free again
+    if (threadIdx.x == 0 && ti + NSLOT < th) KN_ISSUE(ti + NSLOT);
+  }
+#undef KN_ISSUE
+}
+
+// Fallback for NHWC tensors TMA cannot describe (C * es % 16 != 0, e.g. C = 3):
+// thread per (tile, channel pair), direct loads of the halo from global memory.
+template <int DT, int M, int NX, int D>
+__global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typename DType<DT>::T* __restrict__ x, int C,
+                                                                   int H, int W, int pad, int th, int tw, int Cp,
+                                                                   int T, const __grid_constant__ XformParams xp,
+                                                                   typename DType<DT>::T* __restrict__ V,
+                                                                   size_t qstride, size_t plane) {
+  using Tr = DType<DT>;
+  const int pi = blockIdx.x * blockDim.x + threadIdx.x;   // channel pair index
+  const int t = blockIdx.y;
+  if (2 * pi >= Cp) return;
+  const int ca = 2 * pi, cb = ca + 1;
+  const int tj = t % tw, rest = t / tw, ti = rest % th, n = rest / th;
+  float2 rowT[NX][D];
+#pragma unroll
+  for (int a = 0; a < NX; ++a) {
+    const int r = ti * M - pad + a;
+    float2 d[NX];
+#pragma unroll
+    for (int q = 0; q < NX; ++q) {
+      const int c = tj * M - pad + q;
+      const bool ok = r >= 0 && r < H && c >= 0 && c < W;
+      const typename Tr::T* px = x + (((size_t)n * H + (ok ? r : 0)) * W + (ok ? c : 0)) * C;
+      d[q] = make_float2(ok && ca < C ? Tr::load(px + ca) : 0.f, ok && cb < C ? Tr::load(px + cb) : 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < NX; ++q) acc = __ffma2_rn(d[q], make_float2(xp.BT[j][q], xp.BT[j][q]), acc);
+      rowT[a][j] = acc;
+    }
+  }
+  typename Tr::T* out = V + (size_t)t * Cp + ca;
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int a = 0; a < NX; ++a) acc = __ffma2_rn(rowT[a][j], make_float2(xp.BT[i][a], xp.BT[i][a]), acc);
+      store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc, plane);
+    }
+}
+
 // Synchronous variant for rows whose vectors are narrower than 4 bytes (odd W
 // in 16-bit): CTA = (tile-column block, (n, ti), channel block).
 template <int DT, int M, int NX, int D>
@@ -663,10 +855,98 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
   }
 }
 
+// ------------------------------------------------------------------ K4 output transform (NHWC)
+// y[N][Ho][Wo][K].  CTA = 32 tiles (lanes, coalesced M reads along t) x KB
+// output channels (8 warps x KB/8); Y is staged in shared memory as
+// [tile][pixel][channel] in the storage dtype and written back as contiguous
+// runs of KB channels per pixel (16-byte vector stores when K allows).
+// KB output channels per CTA; TS = per-tile stride of the stage in elements
+// (+8: 16-byte aligned rows, and only 4-way bank conflicts for lane = tile)
+template <int M> struct K4N {
+  static constexpr int KB = M <= 4 ? 32 : 16;
+  static constexpr int TS = M * M * KB + 8;
+};
+
+template <int DT, int M, int D>
+__global__ void __launch_bounds__(256) output_transform_nhwc(const float* __restrict__ Mw, int K, int Ho, int Wo,
+                                                             int th, int tw, int T, int Tp,
+                                                             const __grid_constant__ XformParams xp,
+                                                             typename DType<DT>::T* __restrict__ y) {
+  using Tr = DType<DT>;
+  using TT = typename Tr::T;
+  constexpr int KB = K4N<M>::KB, KPW = KB / 8, TS = K4N<M>::TS;
+  extern __shared__ __align__(16) uint8_t k4n_smem[];
+  TT* stage = reinterpret_cast<TT*>(k4n_smem);   // [32 tiles, stride TS][M*M][KB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 32 + lane;
+  const int k0 = blockIdx.y * KB;
+  const size_t qs = (size_t)K * Tp;
+#pragma unroll 1
+  for (int jk = 0; jk < KPW; ++jk) {
+    const int kl = warp * KPW + jk, k = k0 + kl;
+    if (t >= T || k >= K) continue;
+    float Y[M][M];
+#pragma unroll
+    for (int p = 0; p < M; ++p)
+#pragma unroll
+      for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
+    const float* src = Mw + (size_t)k * Tp + t;
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      float Mi[D];
+#pragma unroll
+      for (int j = 0; j < D; ++j) Mi[j] = __ldg(src + (size_t)(i * D + j) * qs);
+      float Z[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        float acc = 0.f;
+#pragma unroll
+        for (int j = 0; j < D; ++j) acc = fmaf(Mi[j], xp.AT[q][j], acc);
+        Z[q] = acc;
+      }
+#pragma unroll
+      for (int p = 0; p < M; ++p)
+#pragma unroll
+        for (int q = 0; q < M; ++q) Y[p][q] = fmaf(xp.AT[p][i], Z[q], Y[p][q]);
+    }
+#pragma unroll
+    for (int p = 0; p < M; ++p)
+#pragma unroll
+      for (int q = 0; q < M; ++q) stage[(size_t)lane * TS + (p * M + q) * KB + kl] = Tr::cvt(Y[p][q]);
+  }
+  __syncthreads();
+  // write-back: units of 8 channels (16 B in 16-bit, 32 B in fp32) per (tile, pixel)
+  constexpr int VE = 8;
+  constexpr int UPP = KB / VE;   // units per pixel
+  const bool vec = (K % VE) == 0 && (reinterpret_cast<uintptr_t>(y) % 16) == 0;
+  for (int u = threadIdx.x; u < 32 * M * M * UPP; u += blockDim.x) {
+    const int tl = u / (M * M * UPP), r = u % (M * M * UPP);
+    const int px = r / UPP, kv = (r % UPP) * VE;
+    const int tt = blockIdx.x * 32 + tl;
+    if (tt >= T || k0 + kv >= K) continue;
+    const int p = px / M, q = px % M;
+    const int tj = tt % tw, rest = tt / tw, ti = rest % th, n = rest / th;
+    const int ho = ti * M + p, wo = tj * M + q;
+    if (ho >= Ho || wo >= Wo) continue;
+    TT* dst = y + (((size_t)n * Ho + ho) * Wo + wo) * K + k0 + kv;
+    const TT* src = stage + (size_t)tl * TS + px * KB + kv;
+    if (vec && k0 + kv + VE <= K) {
+      if constexpr (sizeof(TT) == 2) {
+        *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+      } else {
+        reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(src)[0];
+        reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(src)[1];
+      }
+    } else {
+      for (int e = 0; e < VE && k0 + kv + e < K; ++e) dst[e] = src[e];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launchers
 struct InArgs {
   const void* x;
-  int C, H, W, pad, th, tw, Cp, N;
+  int C, H, W, pad, th, tw, Cp, N, layout;
   const XformParams* xp;
   void* V;
   size_t qstride, plane;
@@ -674,7 +954,7 @@ struct InArgs {
 };
 struct OutArgs {
   const float* Mw;
-  int K, Ho, Wo, th, tw, T, Tp;
+  int K, Ho, Wo, th, tw, T, Tp, layout;
   const XformParams* xp;
   void* y;
   cudaStream_t st;
@@ -683,7 +963,48 @@ using InFn = void (*)(const InArgs&);
 using OutFn = void (*)(const OutArgs&);
 
 template <int DT, int M, int D>
+static void launch_in_nhwc(const InArgs& a) {
+  using TT = typename DType<DT>::T;
+  constexpr int NX = M + 2;
+  const size_t es = sizeof(TT);
+  const CUtensorMapDataType cdt = DT == WINO_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : DT == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                   : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  K1NGeo gk{};
+  gk.C = a.C, gk.H = a.H, gk.W = a.W, gk.pad = a.pad, gk.th = a.th, gk.tw = a.tw, gk.Cp = a.Cp;
+  gk.TJB = a.tw < 8 ? a.tw : 8;
+  while (gk.TJB > 1 && gk.TJB * M + 2 > 256) --gk.TJB;
+  gk.BOXW = gk.TJB * M + 2;
+  gk.box_bytes = (unsigned)(64 * gk.BOXW * NX * es);
+  gk.slot_bytes = (gk.box_bytes + 127) / 128 * 128;
+  gk.NSLOT = 3;
+  while (gk.NSLOT > 2 && 128 + 128 + (size_t)gk.NSLOT * gk.slot_bytes > 110 * 1024) --gk.NSLOT;
+  const size_t smem = 256 + (size_t)gk.NSLOT * gk.slot_bytes;
+  CUtensorMap tm;
+  bool ok = (reinterpret_cast<uintptr_t>(a.x) % 16) == 0 && ((size_t)a.C * es) % 16 == 0 && smem <= 200 * 1024;
+  if (ok) {
+    const uint64_t dims[4] = {(uint64_t)a.C, (uint64_t)a.W, (uint64_t)a.H, (uint64_t)a.N};
+    const uint64_t str[3] = {(uint64_t)a.C * es, (uint64_t)a.W * a.C * es, (uint64_t)a.H * a.W * a.C * es};
+    const uint32_t box[4] = {64, (uint32_t)gk.BOXW, (uint32_t)NX, 1};
+    ok = make_map(&tm, cdt, 4, a.x, dims, str, box, false);
+  }
+  if (ok) {
+    auto kern = input_transform_nhwc<DT, M, NX, D>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
+    kern<<<grid, 32 * gk.TJB, smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
+    return;
+  }
+  const int T = a.N * a.th * a.tw;
+  dim3 grid((a.Cp / 2 + 127) / 128, T);
+  input_transform_nhwc_direct<DT, M, NX, D><<<grid, 128, 0, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th,
+                                                                      a.tw, a.Cp, T, *a.xp, (TT*)a.V, a.qstride,
+                                                                      a.plane);
+}
+
+template <int DT, int M, int D>
 static void launch_in(const InArgs& a) {
+  if (a.layout == WINO_NHWC) return launch_in_nhwc<DT, M, D>(a);
   using TT = typename DType<DT>::T;
   using PT = typename PairT<DT>::T;
   constexpr int NX = M + 2;
@@ -772,6 +1093,15 @@ static void launch_in(const InArgs& a) {
 template <int DT, int M, int D>
 static void launch_out(const OutArgs& a) {
   using Tr = DType<DT>;
+  if (a.layout == WINO_NHWC) {
+    const size_t smem = (size_t)32 * K4N<M>::TS * sizeof(typename Tr::T);
+    constexpr int KB = K4N<M>::KB;
+    auto kern = output_transform_nhwc<DT, M, D>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((a.T + 31) / 32, (a.K + KB - 1) / KB);
+    kern<<<grid, 256, smem, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
+    return;
+  }
   dim3 grid((a.T + 127) / 128, a.K);
   output_transform_nchw<DT, M, D><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp,
                                                           (typename Tr::T*)a.y);

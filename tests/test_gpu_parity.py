@@ -454,3 +454,40 @@ np.save(sys.argv[1], np.concatenate([o.ravel() for o in out]))
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(np.load(f))
     assert np.array_equal(res[0], res[1])
+
+
+NHWC_CASES = [("lin4", "subsolver", 2, 64, 128, 28, 28, 1),     # TMA boxes, 64-channel blocks
+              ("lin4", "subsolver", 2, 72, 40, 19, 23, 1),     # ragged, C = 72 (partial channel block)
+              ("sup1_6", "subsolver", 1, 128, 136, 30, 30, 1),
+              ("lin2", "subsolver", 1, 3, 64, 32, 32, 1),      # C = 3: direct-load fallback
+              ("lin8", "subsolver", 1, 64, 64, 26, 26, 0),
+              ("sup1_4", "residue", 2, 72, 40, 19, 23, 1)]
+
+
+@pytest.mark.parametrize("case", NHWC_CASES, ids=lambda c: f"{c[0]}-{c[1]}-C{c[3]}K{c[4]}-{c[5]}x{c[6]}p{c[7]}")
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+def test_layer_nhwc(case, dtype):
+    """NHWC x and y (wino_layout WINO_NHWC): K1 stages channel-contiguous TMA
+    boxes with no transpose and K4 writes channel runs through shared memory.
+    Same rounding points as NCHW, so y must equal the NCHW result bit for bit,
+    and it is checked against the oracle like every layer."""
+    name, lowering, N, C, K, H, Wd, pad = case
+    a, ref, m = algo_pair(name, lowering)
+    x, w = datagen.layer(N, C, K, H, Wd, dtype, seed=9)
+    xd, wd = dev(x, dtype), dev(w, dtype)
+    y_nchw = W.wino_conv2d(xd, wd, a, pad=pad)
+    y_nhwc = W.wino_conv2d(xd.permute(0, 2, 3, 1).contiguous(), wd, a, pad=pad, layout="nhwc")
+    torch.cuda.synchronize()
+    assert torch.equal(y_nhwc.permute(0, 3, 1, 2), y_nchw)
+    yg = host(y_nhwc.permute(0, 3, 1, 2))
+    yref = CV.direct_conv2d_f64(x, w, pad)
+    if lowering == "subsolver":
+        yo = P.pipeline_conv2d(ref, x, w, dtype, pad)
+    else:
+        yo = P.pipeline_residue_conv2d(ref, x, w, dtype, pad)
+    sg = MT.summary(MT.stats8(yg, yref, m))
+    so = MT.summary(MT.stats8(yo, yref, m))
+    if dtype == "fp32":
+        assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3), sg
+    elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
