@@ -168,7 +168,24 @@ def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
     th, tw = -(-Ho // m), -(-Wo // m)
     T = N * th * tw
     return dict(Ho=Ho, Wo=Wo, th=th, tw=tw, T=T, Tp=-(-T // 32) * 32, Cp=-(-C // 64) * 64, Q=D * D, S=S,
-                planes=2 if dtype == "fp32" else 1)
+                planes=2 if dtype == "fp32" else 1, TB=-(-T // 128), CBW=32 if dtype == "fp32" else 64)
+
+
+def v_to_dense(V, T):
+    """Blocked V [planes][Q][TB][Cp/CBW][128][CBW] (include/wino.h) -> dense
+    [planes][Q][T][Cp] view for inspection (a copy)."""
+    P_, Q, TB, CB, _, CBW = V.shape
+    return V.permute(0, 1, 2, 4, 3, 5).reshape(P_, Q, TB * 128, CB * CBW)[:, :, :T]
+
+
+def v_from_dense(Vd):
+    """Dense [planes][Q][T][Cp] -> the blocked V layout the GEMM reads."""
+    P_, Q, T, Cp = Vd.shape
+    CBW = 32 if Vd.dtype == torch.float32 else 64
+    TB = -(-T // 128)
+    pad = torch.zeros((P_, Q, TB * 128, Cp), dtype=Vd.dtype, device=Vd.device)
+    pad[:, :, :T] = Vd
+    return pad.reshape(P_, Q, TB, 128, Cp // CBW, CBW).permute(0, 1, 2, 4, 3, 5).contiguous()
 
 
 def wino_weight_transform(w, algo, stream=None):
@@ -182,22 +199,23 @@ def wino_weight_transform(w, algo, stream=None):
 
 
 def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
-    """V [planes][Q][T][Cp] in the storage dtype; x [N,C,H,W] or [N,H,W,C] ("nhwc")."""
+    """V [planes][Q][TB][Cp/CBW][128][CBW] (blocked, see v_to_dense) in the storage
+    dtype; x [N,C,H,W] or [N,H,W,C] ("nhwc")."""
     if layout == "nchw":
         N, C, H, W = x.shape
     else:
         N, H, W, C = x.shape
     dt = _TORCH_DT[x.dtype]
     g = geometry(algo, N, C, H, W, 1, pad, dt)
-    V = torch.empty((g["planes"], g["Q"], g["T"], g["Cp"]), dtype=x.dtype, device=x.device)
+    V = torch.empty((g["planes"], g["Q"], g["TB"], g["Cp"] // g["CBW"], 128, g["CBW"]), dtype=x.dtype,
+                    device=x.device)
     check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
                                      _ptr(V), _stream(stream)))
     return V
 
 
-def wino_domain_gemm(V, U, algo, C, K, stream=None):
-    """M [Q][K][Tp] fp32."""
-    T = V.shape[2]
+def wino_domain_gemm(V, U, algo, C, K, T, stream=None):
+    """M [Q][K][Tp] fp32 from blocked V (T tiles) and U."""
     dt = _TORCH_DT[V.dtype]
     Tp = -(-T // 32) * 32
     M = torch.empty((algo.domain ** 2, K, Tp), dtype=torch.float32, device=V.device)

@@ -125,6 +125,7 @@ wino_status wino_domain_gemm(const void* V, const void* U, int T, int C, int K, 
   Geo g = make_geo(al, 1, C, 3, 3, K, 0, dt);  // Cp, Q, S, es, planes
   g.T = T;
   g.Tp = (int)align_up(T, 32);
+  g.TB = (T + 127) / 128;
   return run_domain_gemm(V, U, g, al, dt, M, reinterpret_cast<cudaStream_t>(stream));
 }
 

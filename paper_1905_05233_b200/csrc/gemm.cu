@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-            tma_load_3d(base, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi);
-            if constexpr (kTF32) tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi + Q);
+            tma_load_3d(base, &tmV, &full[stage], 0, 0, (qi * nMB + mb) * KB + kb);   // blocked V: one 16 KB block
+            if constexpr (kTF32)
+              tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], 0, 0, ((qi + Q) * nMB + mb) * KB + kb);
             uint8_t* bb = base + Cfg::NPL * Cfg::A_BYTES;
             tma_load_3d(bb, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
             if constexpr (kTF32) tma_load_3d(bb + Cfg::B_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl + S);
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(512, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-            tma_load_3d(base, &tmV, &full[stage], kb * Cfg::BK, mb * kBM, qi);
+            tma_load_3d(base, &tmV, &full[stage], 0, 0, (qi * nMB + mb) * KB + kb);   // blocked V: one 16 KB block
             tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
             if (++stage == STAGES) stage = 0, phase ^= 1;
           }
@@ -575,7 +576,7 @@ wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, co
   constexpr int BN = 256;
   const uint32_t BK = 128 / (uint32_t)g.es;
   CUtensorMap tv, tu, tm;
-  if (!make_map3(&tv, cdt, g.es, V, g.Cp, g.T, (uint64_t)g.Q * g.planes, BK, kBM) ||
+  if (!make_map3(&tv, cdt, g.es, V, BK, kBM, (uint64_t)g.planes * g.Q * g.TB * (g.Cp / BK), BK, kBM) ||
       !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
       !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, g.T, g.K, g.Q, kBM, 32, false, g.Tp)) {
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
@@ -595,7 +596,7 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
   int BN = tf32 ? (g.K > 64 ? 128 : 64) : (g.K > 128 ? 256 : (g.K > 64 ? 128 : 64));
   const uint32_t BK = 128 / (uint32_t)g.es;
   CUtensorMap tv, tu, tm;
-  if (!make_map3(&tv, cdt, g.es, V, g.Cp, g.T, (uint64_t)g.Q * g.planes, BK, kBM) ||
+  if (!make_map3(&tv, cdt, g.es, V, BK, kBM, (uint64_t)g.planes * g.Q * g.TB * (g.Cp / BK), BK, kBM) ||
       !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
       !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, g.T, g.K, g.Q, kBM, 32, false, g.Tp)) {
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");

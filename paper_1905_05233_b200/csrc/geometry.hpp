@@ -1,5 +1,5 @@
 // geometry.hpp -- layer geometry and workspace layout of wino_conv2d
-// (include/wino.h): U [S][K][Cp] | V [Q][T][Cp] | M [Q][K][Tp] fp32 | group counters.
+// (include/wino.h): U [S][K][Cp] | V [Q][TB][Cp/CBW][128][CBW] | M [Q][K][Tp] fp32 | group counters.
 #pragma once
 #include <cstddef>
 
@@ -13,11 +13,19 @@ struct Geo {
   int N, C, H, W, K, pad;
   int m, D, Q, S;
   int Ho, Wo, th, tw, T, Tp, Cp;
+  int TB, CBW;   // V blocks: 128 tiles x CBW channels (one 128-byte swizzle row per tile)
   size_t es, planes;
   size_t offU, offV, offM, offD, total;
 };
 
 // Tiling of PAPER.md P:498: overlapping (m+2)x(m+2) tiles at stride m.
+// Element offset of V_q[t][c] inside one point plane of the blocked layout:
+// 16 KB blocks [128 t][CBW c], block (t / 128, c / CBW) at ((t/128) * Cp/CBW + c/CBW),
+// so every GEMM A-operand box is one contiguous 16 KB run.
+__host__ __device__ inline size_t v_offset(int t, int c, int Cp, int CBW) {
+  return ((size_t)(t >> 7) * (Cp / CBW) + c / CBW) * (128 * CBW) + (size_t)(t & 127) * CBW + c % CBW;
+}
+
 inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int pad, wino_dtype dt) {
   Geo g;
   g.N = N, g.C = C, g.H = H, g.W = W, g.K = K, g.pad = pad;
@@ -35,7 +43,9 @@ inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int 
   g.es = dt == WINO_F32 ? 4 : 2;
   g.planes = dt == WINO_F32 ? 2 : 1;  // fp32: TF32 hi and lo planes
   size_t u_bytes = g.planes * (size_t)g.S * K * g.Cp * g.es;
-  size_t v_bytes = g.planes * (size_t)g.Q * g.T * g.Cp * g.es;
+  g.TB = (g.T + 127) / 128;
+  g.CBW = (int)(128 / g.es);
+  size_t v_bytes = g.planes * (size_t)g.Q * g.TB * 128 * g.Cp * g.es;
   size_t m_bytes = (size_t)g.Q * K * g.Tp * 4;
   g.offU = 0;
   g.offV = align_up(g.offU + u_bytes, 1024);

@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), 2) inp
         const int tj = tj0 + tjl;
         if (tj >= gk.tw) break;
         const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-        transform_tile_ring<DT, NX, D, PT>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + t * gk.Cp + ca,
+        transform_tile_ring<DT, NX, D, PT>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(TT)),
                                            qstride, plane);
       }
     }
@@ -695,7 +695,8 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
       const int tj = tj0 + tjl;
       if (tj >= gk.tw) break;
       const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-      transform_tile_box<DT, NX, D, PT>(box, gk.BOXW, rowoff, tjl * M + col0 - cst, xp, V + t * gk.Cp + ca, qstride,
+      transform_tile_box<DT, NX, D, PT>(box, gk.BOXW, rowoff, tjl * M + col0 - cst, xp,
+                                        V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(typename DType<DT>::T)), qstride,
                                         plane);
     }
     __syncthreads();   // slot ti % NSLOT is free again
@@ -738,7 +739,7 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
       rowT[a][j] = acc;
     }
   }
-  typename Tr::T* out = V + (size_t)t * Cp + ca;
+  typename Tr::T* out = V + v_offset(t, ca, Cp, 128 / (int)sizeof(typename Tr::T));
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -782,7 +783,8 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
     const int tj = tj0 + tjl;
     if (tj >= tw) break;
     const size_t t = ((size_t)n * th + ti) * tw + tj;
-    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + t * Cp + ca, qstride, plane);
+    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + v_offset((int)t, ca, Cp, 128 / (int)sizeof(TT)),
+                                    qstride, plane);
   }
 }
 

@@ -98,6 +98,8 @@ def test_input_transform(dtype, name, lowering, pad, shape):
     x, _ = datagen.layer(N, C, 1, H, Wd, dtype, seed=4)
     V = W.wino_input_transform(dev(x, dtype), a, pad=pad)
     torch.cuda.synchronize()
+    T_all = CV.tile_grid(H, Wd, m, pad)
+    V = W.v_to_dense(V, N * T_all[2] * T_all[3])
     D = a.domain
     if lowering == "subsolver":
         Vo, _ = P.pipeline_input_transform(ref, x, dtype, pad)
@@ -134,7 +136,7 @@ def test_domain_gemm_isolated(dtype, name, lowering, T_, C, K):
     Uh = np.zeros((1, S, K, Cp))
     Vh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, T_, C)), dtype)
     Uh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, S, K, C)), dtype)
-    M = W.wino_domain_gemm(dev(Vh, dtype), dev(Uh, dtype), a, C, K)
+    M = W.wino_domain_gemm(W.v_from_dense(dev(Vh, dtype)), dev(Uh, dtype), a, C, K, T_)
     torch.cuda.synchronize()
     got = host(M)[:, :, :T_]
     out_pt, in_pt, *_ = a.unit_table()
@@ -155,8 +157,11 @@ def test_domain_gemm_tf32x3():
     xd, wd = dev(x, "fp32"), dev(w, "fp32")
     U = W.wino_weight_transform(wd, a)
     V = W.wino_input_transform(xd, a)
-    M = W.wino_domain_gemm(V, U, a, 96, 48)
+    T_all = CV.tile_grid(14, 18, 4, 1)
+    T0 = T_all[2] * T_all[3]
+    M = W.wino_domain_gemm(V, U, a, 96, 48, T0)
     torch.cuda.synchronize()
+    V = W.v_to_dense(V, T0)
     Uf = (host(U[0]) + host(U[1]))[:, :, :96]
     Vf = (host(V[0]) + host(V[1]))[:, :, :96]
     T_ = Vf.shape[1]
