@@ -90,11 +90,49 @@ wino_status wino_conv2d_host_io(const void* x_host, void* x_dev, const void* w_d
   if (!x_host || !out_host || !x_dev || !out_dev) return set_last_error("NULL buffer"), WINO_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Geo g = make_geo(al, N, C, H, W, K, pad, dt);
-  size_t xb = (size_t)N * C * H * W * g.es, yb = (size_t)N * K * g.Ho * g.Wo * g.es;
-  WINO_CUDA_CHECK(cudaMemcpyAsync(x_dev, x_host, xb, cudaMemcpyHostToDevice, st));
-  s = wino_conv2d(x_dev, w_dev, N, C, H, W, K, pad, al, dt, layout, out_dev, ws, ws_bytes, stream);
-  if (s != WINO_OK) return s;
-  WINO_CUDA_CHECK(cudaMemcpyAsync(out_host, out_dev, yb, cudaMemcpyDeviceToHost, st));
+  if (ws_bytes < g.total) return set_last_error("workspace too small"), WINO_E_WORKSPACE;
+  // Images are independent (P:498 tiles never cross images), so the batch is
+  // processed in (up to 8) chunks: the H2D copy of chunk j+1 and the D2H copy of chunk
+  // j-1 (two library-owned copy streams, opposite PCIe directions) overlap the
+  // layer on chunk j (the caller's stream).  The caller's stream finally waits
+  // for the last copy, so synchronising it covers everything.
+  const size_t xi = (size_t)C * H * W * g.es, yi = (size_t)K * g.Ho * g.Wo * g.es;   // bytes per image
+  const int nch = N >= 8 ? 8 : N;
+  static thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
+  static thread_local cudaEvent_t ev[2][16];
+  if (!s_in) {
+    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    for (int a = 0; a < 2; ++a)
+      for (int j = 0; j < 16; ++j) WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev[a][j], cudaEventDisableTiming));
+  }
+  // copies must not start before work already queued on the caller's stream
+  cudaEvent_t start = ev[1][15];
+  WINO_CUDA_CHECK(cudaEventRecord(start, st));
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(s_in, start, 0));
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(s_out, start, 0));
+  int launches = 0;
+  for (int j = 0, n0 = 0; j < nch; ++j) {
+    const int nj = N / nch + (j < N % nch ? 1 : 0);
+    char* xd = static_cast<char*>(x_dev) + (size_t)n0 * xi;
+    char* yd = static_cast<char*>(out_dev) + (size_t)n0 * yi;
+    WINO_CUDA_CHECK(cudaMemcpyAsync(xd, static_cast<const char*>(x_host) + (size_t)n0 * xi, (size_t)nj * xi,
+                                    cudaMemcpyHostToDevice, s_in));
+    WINO_CUDA_CHECK(cudaEventRecord(ev[0][j], s_in));
+    WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev[0][j], 0));
+    s = wino_conv2d(xd, w_dev, nj, C, H, W, K, pad, al, dt, layout, yd, ws, ws_bytes, stream);
+    if (s != WINO_OK) return s;
+    launches += wino_last_launch_count();
+    WINO_CUDA_CHECK(cudaEventRecord(ev[1][j], st));
+    WINO_CUDA_CHECK(cudaStreamWaitEvent(s_out, ev[1][j], 0));
+    WINO_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(out_host) + (size_t)n0 * yi, yd, (size_t)nj * yi,
+                                    cudaMemcpyDeviceToHost, s_out));
+    n0 += nj;
+  }
+  WINO_CUDA_CHECK(cudaEventRecord(ev[0][15], s_out));
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev[0][15], 0));
+  reset_launch_count();
+  count_launch(launches);
   return WINO_OK;
 }
 

@@ -496,3 +496,26 @@ def test_layer_nhwc(case, dtype):
         assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3), sg
     elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
+
+
+@pytest.mark.parametrize("N,layout", [(19, "nchw"), (3, "nchw"), (9, "nhwc")])
+def test_host_io_chunked_equals_device_call(N, layout):
+    """wino_conv2d_host_io (pinned host x -> device -> layer -> pinned host y,
+    processed in up to 8 image chunks with the copies overlapping the layer)
+    returns exactly the device call's y, for ragged chunk splits."""
+    a, ref, m = algo_pair("lin4")
+    x, w = datagen.layer(N, 64, 136, 14, 18, "bf16", seed=12)
+    xd, wd = dev(x, "bf16"), dev(w, "bf16")
+    if layout == "nhwc":
+        xd = xd.permute(0, 2, 3, 1).contiguous()
+    y_dev = W.wino_conv2d(xd, wd, a, layout=layout)
+    xh = torch.empty(xd.shape, dtype=xd.dtype, pin_memory=True)
+    xh.copy_(xd.cpu())
+    x2 = torch.empty_like(xd)
+    y2 = torch.empty_like(y_dev)
+    yh = torch.empty(y_dev.shape, dtype=y_dev.dtype, pin_memory=True)
+    yh.zero_()
+    ws = W.alloc_workspace(W.wino_conv2d_workspace(a, N, 64, 14, 18, 136, 1, "bf16", layout))
+    W.wino_conv2d_host_io(xh, x2, wd, a, y2, yh, ws, layout=layout)
+    torch.cuda.synchronize()
+    assert torch.equal(yh, y_dev.cpu())
