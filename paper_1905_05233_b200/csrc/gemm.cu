@@ -57,7 +57,9 @@ __global__ void __launch_bounds__(256, 1)
                        uint32_t idesc, const __grid_constant__ GemmSched gs) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned for the 128-byte swizzle atoms; offsetting the shared array keeps
+  // a shared-space pointer (STS / LDS, no generic stores and CTA-wide MEMBARs)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
@@ -301,7 +303,9 @@ __global__ void __launch_bounds__(512, 1)
                              const __grid_constant__ GemmSched gs, const __grid_constant__ FuseArgs fa) {
   using Cfg = GemmCfg<false, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned for the 128-byte swizzle atoms; offsetting the shared array keeps
+  // a shared-space pointer (STS / LDS, no generic stores and CTA-wide MEMBARs)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
