@@ -45,8 +45,10 @@ struct GemmCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int EPI_BUFS = 2;
   static constexpr int EPI_BYTES = 32 * kBM * 4;   // one [32 k][128 t] fp32 box
+  // as many epilogue staging buffers (TMA stores in flight) as shared memory allows, 2..4
+  static constexpr int EPI_FREE = (227 * 1024 - STAGES * STAGE_BYTES - 1024 - 256) / EPI_BYTES;
+  static constexpr int EPI_BUFS = EPI_FREE > 4 ? 4 : (EPI_FREE < 2 ? 2 : EPI_FREE);
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BUFS * EPI_BYTES + 1024 + 256;
 };
 
@@ -612,7 +614,7 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
     if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, st);
     return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, st);
   }
-  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, st);
+  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, st);   // 3 stages + 4 epilogue buffers: 8 % slower
   if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, st);
   return launch_gemm<false, 64, 8>(tv, tu, tm, g, al->gs, fmt, st);
 }
