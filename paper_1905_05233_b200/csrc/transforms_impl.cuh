@@ -668,22 +668,31 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
   const int tj0 = blockIdx.x * gk.TJB, n = blockIdx.y, c0 = blockIdx.z * 64;
   const int col0 = tj0 * M - pad, cst = col0 < 0 ? 0 : col0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // warps 0 .. nw-2 transform tiles; warp nw-1 is the TMA producer.  Slots are
+  // released per warp through `empty` mbarriers, so compute warps never wait
+  // for each other -- only for their data.
+  uint64_t* empty = full + NSLOT;
+  const int cw = nw - 1;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], cw);
     fence_barrier_init();
     tma_prefetch(&tmx);
   }
   __syncthreads();
-#define KN_ISSUE(ti_)                                                                                        \
-  do {                                                                                                       \
-    const int s_ = (ti_) % NSLOT;                                                                            \
-    const int g_ = (ti_) * M - pad;                                                                          \
-    fence_proxy_async_shared();                                                                              \
-    mbar_arrive_expect_tx(&full[s_], gk.box_bytes);                                                          \
-    tma_load_4d(slots + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], c0, cst, g_ < 0 ? 0 : g_, n);           \
-  } while (0)
-  if (threadIdx.x == 0)
-    for (int ti = 0; ti < NSLOT && ti < th; ++ti) KN_ISSUE(ti);
+  if (warp == cw) {
+    if (lane == 0) {
+#pragma unroll 1
+      for (int ti = 0; ti < th; ++ti) {
+        const int s_ = ti % NSLOT;
+        if (ti >= NSLOT) mbar_wait(&empty[s_], (uint32_t)(((ti / NSLOT) - 1) & 1));
+        const int g_ = ti * M - pad;
+        fence_proxy_async_shared();
+        mbar_arrive_expect_tx(&full[s_], gk.box_bytes);
+        tma_load_4d(slots + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], c0, cst, g_ < 0 ? 0 : g_, n);
+      }
+    }
+    return;
+  }
   const int ca = c0 + 2 * lane;
 #pragma unroll 1
   for (int ti = 0; ti < th; ++ti) {
@@ -691,7 +700,7 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
     const PT* box = reinterpret_cast<const PT*>(slots + (size_t)(ti % NSLOT) * gk.slot_bytes) + lane;
     const int g = ti * M - pad;
     const int rowoff = g - (g < 0 ? 0 : g);   // -pad for the first tile row, else 0
-    for (int tjl = warp; tjl < gk.TJB; tjl += nw) {
+    for (int tjl = warp; tjl < gk.TJB; tjl += cw) {
       const int tj = tj0 + tjl;
       if (tj >= gk.tw) break;
       const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
@@ -699,10 +708,9 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
                                         V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(typename DType<DT>::T)), qstride,
                                         plane);
     }
-    __syncthreads();   // slot ti % NSLOT is free again
-    if (threadIdx.x == 0 && ti + NSLOT < th) KN_ISSUE(ti + NSLOT);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[ti % NSLOT]);   // this warp is done with the slot
   }
-#undef KN_ISSUE
 }
 
 // Fallback for NHWC tensors TMA cannot describe (C * es % 16 != 0, e.g. C = 3):
@@ -974,12 +982,12 @@ static void launch_in_nhwc(const InArgs& a) {
                                                    : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   K1NGeo gk{};
   gk.C = a.C, gk.H = a.H, gk.W = a.W, gk.pad = a.pad, gk.th = a.th, gk.tw = a.tw, gk.Cp = a.Cp;
-  gk.TJB = a.tw < 8 ? a.tw : 8;
+  gk.TJB = a.tw < 7 ? a.tw : 7;   // one compute warp per tile
   while (gk.TJB > 1 && gk.TJB * M + 2 > 256) --gk.TJB;
   gk.BOXW = gk.TJB * M + 2;
   gk.box_bytes = (unsigned)(64 * gk.BOXW * NX * es);
   gk.slot_bytes = (gk.box_bytes + 127) / 128 * 128;
-  gk.NSLOT = 3;
+  gk.NSLOT = 4;
   while (gk.NSLOT > 2 && 128 + 128 + (size_t)gk.NSLOT * gk.slot_bytes > 110 * 1024) --gk.NSLOT;
   const size_t smem = 256 + (size_t)gk.NSLOT * gk.slot_bytes;
   CUtensorMap tm;
@@ -994,7 +1002,8 @@ static void launch_in_nhwc(const InArgs& a) {
     auto kern = input_transform_nhwc<DT, M, NX, D>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
-    kern<<<grid, 32 * gk.TJB, smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
+    const int cw = gk.TJB < 7 ? gk.TJB : 7;   // compute warps (+1 TMA producer warp)
+    kern<<<grid, 32 * (cw + 1), smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
     return;
   }
   const int T = a.N * a.th * a.tw;
