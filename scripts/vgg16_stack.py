@@ -1,0 +1,86 @@
+"""BASELINE cfg4: the VGG-16 conv stack (13 conv 3x3 layers, 64 -> 512 channels,
+2x2 max-pool between blocks, ReLU after each conv; reading A16) on a
+synthetic batch N=64 of 224x224x3 U[0,1) images with He-normal weights, bf16,
+for F(4x4) / F(6x6) linear vs superlinear sets.  Per layer: the Winograd layer
+time (CUDA events, wino_conv2d incl. its weight transform) and the error vs the
+fp64 direct convolution on the device (on a 2-image sample, chained on the
+Winograd activations).  ReLU / max-pool between layers are torch glue, not timed.
+
+    python scripts/vgg16_stack.py [--n 64] [--algos lin4,sup1_4,lin6,sup1_6] > profiles/vgg16_stack_r01.json
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+STACK = [(3, 64), (64, 64), "pool", (64, 128), (128, 128), "pool", (128, 256), (256, 256), (256, 256), "pool",
+         (256, 512), (512, 512), (512, 512), "pool", (512, 512), (512, 512), (512, 512)]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--algos", default="lin4,sup1_4,lin6,sup1_6")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sample", type=int, default=2)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1905_05233_b200 as Wn
+    from paper_1905_05233_b200.algos import canonical_spec
+    dt, tdt = "bf16", torch.bfloat16
+    rng = np.random.default_rng(0)
+    x0 = torch.from_numpy(rng.random((a.n, 3, 224, 224))).to(tdt).cuda()
+    weights = []
+    for layer in STACK:
+        if layer != "pool":
+            cin, cout = layer
+            w = rng.normal(0.0, datagen.he_sigma(cin), (cout, cin, 3, 3))
+            weights.append(torch.from_numpy(w).to(tdt).cuda())
+    out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, bf16, "
+                       f"error on {a.sample} images vs fp64 direct", "algos": {}}
+    st = torch.cuda.current_stream()
+    for name in a.algos.split(","):
+        spec, m = canonical_spec(name)
+        algo = Wn.WinoAlgo(spec, m)
+        act = x0
+        rows, li, total = [], 0, 0.0
+        for layer in STACK:
+            if layer == "pool":
+                act = torch.nn.functional.max_pool2d(act, 2)
+                continue
+            w = weights[li]
+            N, C, H, W = act.shape
+            K = w.shape[0]
+            ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, N, C, H, W, K, 1, dt))
+            y = torch.empty((N, K, H, W), dtype=tdt, device="cuda")
+            Wn.wino_conv2d(act, w, algo, out=y, workspace=ws, stream=st)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(a.reps):
+                Wn.wino_conv2d(act, w, algo, out=y, workspace=ws, stream=st)
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.reps
+            total += ms
+            xs = act[:a.sample].contiguous()
+            yref = Wn.wino_direct_conv2d_f64(xs, w, 1, stream=st)
+            s = Wn.summary(Wn.wino_error_stats(y[:a.sample].contiguous(), yref, m, stream=st).cpu())
+            flops = 2.0 * N * K * C * 9 * H * W
+            rows.append({"layer": li + 1, "C": C, "K": K, "HW": H, "ms": ms, "tflops_direct_eq": flops / ms / 1e9,
+                         "rel_l1": s["rel_l1"], "mean_rel": s["mean_rel"], "nonfinite": s["nonfinite"]})
+            del ws, yref
+            act = torch.relu(y)
+            li += 1
+        out["algos"][name] = {"spec": spec, "m": m, "mu": algo.mu, "layers": rows, "total_ms": total}
+        torch.cuda.empty_cache()
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
