@@ -36,6 +36,50 @@ template <> struct DType<WINO_BF16> {
 
 inline size_t dtype_size(wino_dtype dt) { return dt == WINO_F32 ? 4 : 2; }
 
+// Store one output-tile row v[0..M) (rounded to the storage dtype) at row[0..valid)
+// with the widest naturally aligned vector stores (16 / 8 / 4 bytes); ragged or
+// unaligned rows fall back to element stores.  (A 6-wide bf16 row is 12 bytes:
+// three 4-byte stores instead of six 2-byte ones.)
+template <typename Tr, int M>
+__device__ __forceinline__ void store_tile_row(typename Tr::T* row, const float (&v)[M], int valid) {
+  using TT = typename Tr::T;
+  constexpr int RB = M * (int)sizeof(TT);
+  union {
+    TT e[M];
+    uint32_t u[(RB + 3) / 4];
+  } pk;
+#pragma unroll
+  for (int q = 0; q < M; ++q) pk.e[q] = Tr::cvt(v[q]);
+  const uintptr_t a = reinterpret_cast<uintptr_t>(row);
+  if constexpr (RB % 4 == 0) {
+    if (valid >= M) {
+      if constexpr (RB % 16 == 0) {
+        if (a % 16 == 0) {
+#pragma unroll
+          for (int c = 0; c < RB / 16; ++c)
+            reinterpret_cast<uint4*>(row)[c] = make_uint4(pk.u[4 * c], pk.u[4 * c + 1], pk.u[4 * c + 2], pk.u[4 * c + 3]);
+          return;
+        }
+      }
+      if constexpr (RB % 8 == 0) {
+        if (a % 8 == 0) {
+#pragma unroll
+          for (int c = 0; c < RB / 8; ++c) reinterpret_cast<uint2*>(row)[c] = make_uint2(pk.u[2 * c], pk.u[2 * c + 1]);
+          return;
+        }
+      }
+      if (a % 4 == 0) {
+#pragma unroll
+        for (int c = 0; c < RB / 4; ++c) reinterpret_cast<uint32_t*>(row)[c] = pk.u[c];
+        return;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < M; ++q)
+    if (q < valid) row[q] = pk.e[q];
+}
+
 // Split an fp32 value into TF32 hi (round to nearest, 10-bit mantissa) and the
 // exact fp32 remainder lo = v - hi (the MMA reads lo's top 11 bits).
 __device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {

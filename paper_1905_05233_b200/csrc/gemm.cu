@@ -35,7 +35,7 @@ namespace wino {
 
 constexpr int kBM = 128;
 
-template <bool kTF32, int BN, int STAGES>
+template <bool kTF32, int BN, int STAGES, int EPI = 0>
 struct GemmCfg {
   static constexpr int ES = kTF32 ? 4 : 2;
   static constexpr int BK = 128 / ES;   // elements per 128-byte swizzled row
@@ -48,7 +48,7 @@ struct GemmCfg {
   static constexpr int EPI_BYTES = 32 * kBM * 4;   // one [32 k][128 t] fp32 box
   // as many epilogue staging buffers (TMA stores in flight) as shared memory allows, 2..4
   static constexpr int EPI_FREE = (227 * 1024 - STAGES * STAGE_BYTES - 1024 - 256) / EPI_BYTES;
-  static constexpr int EPI_BUFS = EPI_FREE > 4 ? 4 : (EPI_FREE < 2 ? 2 : EPI_FREE);
+  static constexpr int EPI_BUFS = EPI ? EPI : (EPI_FREE > 4 ? 4 : (EPI_FREE < 2 ? 2 : EPI_FREE));
   static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BUFS * EPI_BYTES + 1024 + 256;
 };
 
@@ -213,6 +213,7 @@ struct FuseArgs {
   int nKS;              // 32-channel slices of K
   int need;             // point-GEMM items per tile block (= Q * nNB)
   void* y;
+  const float* M;       // the M workspace (for the L2 discards)
   int* done;            // [nMB] point-GEMM items stored, per tile block (zeroed before the launch)
   int* fixed;           // [nMB] fixup items finished, per tile block (zeroed before the launch)
   int lag;              // the producer starts tile block mb only once block mb - lag is fully fixed up
@@ -230,80 +231,61 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
+// Output transform of one (tile t, channel k) from the TMA-staged M piece
+// fb[q][128 t] (all Q points of channel k for the 128-tile block): Y = A^T M A,
+// same fp32 operation order as K4 (output_transform_nchw).
 template <int DT, int M, int D>
-__device__ __forceinline__ void fixup_item(const float* __restrict__ Mw, const FuseArgs& fa, int mb, int ks, int tid) {
+__device__ __forceinline__ void fixup_point(const float* fb, const FuseArgs& fa, int t, int tl, int k) {
   using Tr = DType<DT>;
   using TT = typename Tr::T;
-  const int t = mb * kBM + (tid & (kBM - 1));
-  const int kh = tid >> 7;   // 256 fixup threads: two halves of the 32-channel slice
-  const int k0 = ks * 32 + kh * 16, k1 = min(fa.K, k0 + 16);
-  if (t >= fa.T) return;
   const int tj = t % fa.tw, rest = t / fa.tw;
   const int ti = rest % fa.th, n = rest / fa.th;
-  const size_t qs = (size_t)fa.K * fa.Tp;
-  constexpr int RB = M * (int)sizeof(TT);
-  constexpr bool kVec = (RB == 4 || RB == 8 || RB == 16);
-  const bool vec = kVec && tj * M + M <= fa.Wo && ((fa.Wo * (int)sizeof(TT)) % RB) == 0 &&
-                   (reinterpret_cast<uintptr_t>(fa.y) % RB) == 0;
-#pragma unroll 1
-  for (int k = k0; k < k1; ++k) {
-    const float* src = Mw + (size_t)k * fa.Tp + t;
-    float Y[M][M];
+  float Y[M][M];
+#pragma unroll
+  for (int p = 0; p < M; ++p)
+#pragma unroll
+    for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    float v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = fb[(i * D + j) * kBM + tl];
+    float Z[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      float acc = 0.f;
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc = fmaf(v[j], fa.AT[q][j], acc);
+      Z[q] = acc;
+    }
 #pragma unroll
     for (int p = 0; p < M; ++p)
 #pragma unroll
-      for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
+      for (int q = 0; q < M; ++q) Y[p][q] = fmaf(fa.AT[p][i], Z[q], Y[p][q]);
+  }
+  TT* dst = reinterpret_cast<TT*>(fa.y) + (((size_t)n * fa.K + k) * fa.Ho + (size_t)ti * M) * fa.Wo + (size_t)tj * M;
 #pragma unroll
-    for (int i = 0; i < D; ++i) {
-      float v[D];
-#pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = __ldcg(src + (size_t)(i * D + j) * qs);
-      float Z[M];
-#pragma unroll
-      for (int q = 0; q < M; ++q) {
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 0; j < D; ++j) acc = fmaf(v[j], fa.AT[q][j], acc);
-        Z[q] = acc;
-      }
-#pragma unroll
-      for (int p = 0; p < M; ++p)
-#pragma unroll
-        for (int q = 0; q < M; ++q) Y[p][q] = fmaf(fa.AT[p][i], Z[q], Y[p][q]);
-    }
-    TT* dst = reinterpret_cast<TT*>(fa.y) + (((size_t)n * fa.K + k) * fa.Ho + (size_t)ti * M) * fa.Wo + (size_t)tj * M;
-#pragma unroll
-    for (int p = 0; p < M; ++p) {
-      if (ti * M + p >= fa.Ho) break;
-      TT* row = dst + (size_t)p * fa.Wo;
-      if constexpr (kVec) {
-        if (vec) {
-          union {
-            TT e[M];
-            uint32_t u[RB / 4];
-          } pk;
-#pragma unroll
-          for (int q = 0; q < M; ++q) pk.e[q] = Tr::cvt(Y[p][q]);
-          if constexpr (RB == 4) *reinterpret_cast<uint32_t*>(row) = pk.u[0];
-          if constexpr (RB == 8) *reinterpret_cast<uint2*>(row) = make_uint2(pk.u[0], pk.u[1]);
-          if constexpr (RB == 16) *reinterpret_cast<uint4*>(row) = make_uint4(pk.u[0], pk.u[1], pk.u[2], pk.u[3]);
-          continue;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < M; ++q)
-        if (tj * M + q < fa.Wo) row[q] = Tr::cvt(Y[p][q]);
-    }
+  for (int p = 0; p < M; ++p) {
+    if (ti * M + p >= fa.Ho) break;
+    store_tile_row<Tr, M>(dst + (size_t)p * fa.Wo, Y[p], fa.Wo - tj * M);
   }
 }
 
+constexpr int kFuseStages = 3;   // GEMM stages of the fused kernel (room for the M pieces)
+template <int BN>
+using FusedCfg = GemmCfg<false, BN, kFuseStages, 2>;
+// shared memory of the fused kernel: GEMM stages + 2 epilogue boxes + barriers,
+// then two M pieces of Q x 128 fp32 (one channel of every point for a 128-tile block)
+template <int BN>
+constexpr int fused_smem(int Q) { return FusedCfg<BN>::SMEM + 128 + 2 * Q * kBM * 4; }
+
 template <int BN, int STAGES, int DT, int MO, int DO>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(384, 1)
     domain_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
-                             const __grid_constant__ CUtensorMap tmM, const float* __restrict__ Mw, int T, int K,
-                             int Cp, int nMB, int nNB, int Q, int S, uint32_t idesc,
+                             const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmMl,
+                             int T, int K, int Cp, int nMB, int nNB, int Q, int S, uint32_t idesc,
                              const __grid_constant__ GemmSched gs, const __grid_constant__ FuseArgs fa) {
-  using Cfg = GemmCfg<false, BN, STAGES>;
+  using Cfg = GemmCfg<false, BN, STAGES, 2>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned for the 128-byte swizzle atoms; offsetting the shared array keeps
   // a shared-space pointer (STS / LDS, no generic stores and CTA-wide MEMBARs)
@@ -313,15 +295,20 @@ __global__ void __launch_bounds__(512, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ffull = tempty + 2;    // [2] M piece landed (TMA)
+  uint64_t* fempty = ffull + 2;    // [2] M piece consumed (128 fixup threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + 2);
+  float* fbuf = reinterpret_cast<float*>(smem + Cfg::SMEM - 1024 + 128);   // 2 x [Q][128] fp32
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmV);
     tma_prefetch(&tmU);
     tma_prefetch(&tmM);
+    tma_prefetch(&tmMl);
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
+    for (int a = 0; a < 2; ++a) mbar_init(&ffull[a], 1), mbar_init(&fempty[a], kBM);
     fence_barrier_init();
     fence_proxy_async_shared();
   }
@@ -443,25 +430,50 @@ __global__ void __launch_bounds__(512, 1)
     if (storer) bulk_wait_all();
   } else if (warp >= 8) {
     // -------------------------------------------------- fixup warps: output transform from L2
-    const int tid = threadIdx.x - 256;   // 256 fixup threads
+    // Fixup item (mb, ks): channels [32 ks, 32 ks + 32) of tile block mb.  One
+    // thread streams the item's M pieces (all Q points of one channel k, 128
+    // tiles: a {128, 1, Q} TMA box of M) through two shared-memory buffers;
+    // thread tl computes tile mb*128 + tl.  Consumed M lines are discarded
+    // from L2 (no write-back), and the block's `fixed` counter releases the
+    // producer's backpressure.
+    const int tl = threadIdx.x - 256;
+    const bool issuer = tl == 0;
     const int nFix = nMB * fa.nKS;
+    const uint32_t piece_bytes = (uint32_t)fa.Q * kBM * 4;
+    const size_t qs = (size_t)fa.K * fa.Tp;
+    int piece = 0;   // running piece counter (buffer = piece & 1, use = piece >> 1)
     for (int f = blockIdx.x; f < nFix; f += gridDim.x) {
       const int mb = f / fa.nKS, ks = f % fa.nKS;
-      if (lane == 0)
-        while (ld_acquire(fa.done + mb) < fa.need) __nanosleep(256);
-      __syncwarp();
-      fixup_item<DT, MO, DO>(Mw, fa, mb, ks, tid);
-      named_bar_sync(2, 256);
-      // every M line of (all points, 32 channels, this 128-tile block) has been read: drop it from L2
       const int k0 = ks * 32, nk = min(fa.K, k0 + 32) - k0;
-      const int lines = fa.Q * nk * 4;
-      for (int l = tid; l < lines; l += 256) {
-        const int q = l / (nk * 4), r = l % (nk * 4);
-        const float* ptr = Mw + ((size_t)q * fa.K + k0 + r / 4) * fa.Tp + (size_t)mb * kBM + (r % 4) * 32;
-        discard_l2(ptr);
+      if (issuer) {
+        while (ld_acquire(fa.done + mb) < fa.need) __nanosleep(256);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        for (int j = 0; j < 2 && j < nk; ++j) {
+          const int pc = piece + j, b = pc & 1;
+          if (pc >= 2) mbar_wait(&fempty[b], (uint32_t)(((pc >> 1) - 1) & 1));
+          mbar_arrive_expect_tx(&ffull[b], piece_bytes);
+          tma_load_3d(fbuf + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + j, 0);
+        }
       }
-      named_bar_sync(2, 256);
-      if (tid == 0) {
+      for (int j = 0; j < nk; ++j, ++piece) {
+        const int b = piece & 1;
+        mbar_wait(&ffull[b], (uint32_t)((piece >> 1) & 1));
+        const float* fb = fbuf + (size_t)b * fa.Q * kBM;
+        // the piece is in shared memory: its L2 lines (Q rows x 512 B) can go
+        for (int l = tl; l < fa.Q * 4; l += kBM)
+          discard_l2(fa.M + (size_t)(l >> 2) * qs + (size_t)(k0 + j) * fa.Tp + (size_t)mb * kBM + (l & 3) * 32);
+        const int t = mb * kBM + tl;
+        if (t < fa.T) fixup_point<DT, MO, DO>(fb, fa, t, tl, k0 + j);
+        mbar_arrive(&fempty[b]);
+        if (issuer && j + 2 < nk) {
+          const int pc = piece + 2;
+          mbar_wait(&fempty[b], (uint32_t)(((pc >> 1) - 1) & 1));
+          mbar_arrive_expect_tx(&ffull[b], piece_bytes);
+          tma_load_3d(fbuf + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + j + 2, 0);
+        }
+      }
+      named_bar_sync(2, kBM);
+      if (issuer) {
         __threadfence();
         red_release_add(fa.fixed + mb, 1);
       }
@@ -509,23 +521,30 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
 template <int DT, int MO, int DO>
 static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
                                 const wino_algo* al, uint32_t fmt, const float* M, void* y, int* done, cudaStream_t st) {
-  constexpr int BN = 256, STAGES = 4;
-  using Cfg = GemmCfg<false, BN, STAGES>;
+  constexpr int BN = 256, STAGES = kFuseStages;
   auto kern = domain_gemm_fused_kernel<BN, STAGES, DT, MO, DO>;
-  static bool attr = false;
-  if (!attr) {
-    WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
-    attr = true;
-  }
+  const int smem = fused_smem<BN>(g.Q);
+  WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
+  // M pieces for the fixup warps: box {128 t, 1 k, Q points} of M [Q][K][Tp]
+  CUtensorMap tml;
+  {
+    const uint64_t dims[3] = {(uint64_t)g.Tp, (uint64_t)g.K, (uint64_t)g.Q};
+    const uint64_t str[2] = {(uint64_t)g.Tp * 4, (uint64_t)g.K * g.Tp * 4};
+    const uint32_t box[3] = {(uint32_t)kBM, 1, (uint32_t)g.Q};
+    if (!make_map(&tml, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, M, dims, str, box, false)) {
+      set_last_error("cuTensorMapEncodeTiled failed for the fused M pieces");
+      return WINO_E_CUDA;
+    }
+  }
   FuseArgs fa{};
   for (int q = 0; q < al->m; ++q)
     for (int j = 0; j < al->D; ++j) fa.AT[q][j] = al->xp.AT[q][j];
   fa.D = al->D, fa.Q = g.Q, fa.K = g.K, fa.T = g.T, fa.Tp = g.Tp, fa.Ho = g.Ho, fa.Wo = g.Wo, fa.th = g.th,
-  fa.tw = g.tw, fa.nKS = (g.K + 31) / 32, fa.need = al->gs.Q * nNB, fa.y = y, fa.done = done;
+  fa.tw = g.tw, fa.nKS = (g.K + 31) / 32, fa.need = al->gs.Q * nNB, fa.y = y, fa.M = M, fa.done = done;
   fa.fixed = done + nMB;
-  // tile blocks of M (Q * K * 128 * 4 bytes each) allowed in flight: ~40 MB of the 126 MB L2
   {
+    // tile blocks of M (Q * K * 128 * 4 bytes each) allowed in flight
     const size_t blk = (size_t)g.Q * g.K * kBM * 4;
     int lag = (int)((40u << 20) / (blk ? blk : 1));
     fa.lag = lag < 2 ? 2 : lag;
@@ -534,16 +553,14 @@ static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, co
   WINO_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * 2 * nMB, st));
   const int items = al->gs.Q * nMB * nNB;
   int grid = items < num_sms() ? items : num_sms();
-  const int nfix = nMB * fa.nKS;
   if (grid < 1) grid = 1;
-  (void)nfix;
   const uint32_t idesc = make_idesc(fmt, kBM, BN);
   int T = g.T, K = g.K, Cp = g.Cp, Q = al->gs.Q, S = g.S;
-  const float* Mp = M;
-  void* args[] = {(void*)&tv, (void*)&tu, (void*)&tm, (void*)&Mp, &T, &K, &Cp, (void*)&nMB, (void*)&nNB, &Q, &S,
+  int nMBv = nMB, nNBv = nNB;
+  void* args[] = {(void*)&tv, (void*)&tu, (void*)&tm, (void*)&tml, &T, &K, &Cp, (void*)&nMBv, (void*)&nNBv, &Q, &S,
                   (void*)&idesc, (void*)&al->gs, (void*)&fa};
   // cooperative launch: every CTA is resident (the fixup warps wait on other CTAs' items)
-  WINO_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(512), args, Cfg::SMEM, st));
+  WINO_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(384), args, smem, st));
   WINO_LAUNCH_CHECK();
   return WINO_OK;
 }
@@ -578,6 +595,7 @@ wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, co
                                   float* M, void* y, int* done, cudaStream_t st) {
   const int doff = al->D - al->m - 2;
   if (dt == WINO_F32 || g.K <= 128 || al->m < 2 || al->m > 8 || doff < 0 || doff > 2) return WINO_E_UNSUPPORTED;
+  if (fused_smem<256>(g.Q) > 227 * 1024) return WINO_E_UNSUPPORTED;   // the M pieces must fit (Q <= 49)
   CUtensorMapDataType cdt = dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   constexpr int BN = 256;
   const uint32_t BK = 128 / (uint32_t)g.es;

@@ -836,32 +836,89 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
   const int tj = t % tw, rest = t / tw;
   const int ti = rest % th, n = rest / th;
   typename Tr::T* dst = y + (((size_t)n * K + k) * Ho + (size_t)ti * M) * Wo + (size_t)tj * M;
-  // full-width tile rows are stored as one vector when the row is aligned
-  constexpr int RB = M * (int)sizeof(typename Tr::T);
-  constexpr bool kVec = (RB == 4 || RB == 8 || RB == 16);
-  const bool vec = kVec && tj * M + M <= Wo && ((Wo * (int)sizeof(typename Tr::T)) % RB) == 0 &&
-                   (reinterpret_cast<uintptr_t>(y) % RB) == 0;
 #pragma unroll
   for (int p = 0; p < M; ++p) {
     if (ti * M + p >= Ho) break;
-    typename Tr::T* row = dst + (size_t)p * Wo;
-    if constexpr (kVec) {
-      if (vec) {
-        union {
-          typename Tr::T e[M];
-          uint32_t u[RB / 4];
-        } pk;
-#pragma unroll
-        for (int q = 0; q < M; ++q) pk.e[q] = Tr::cvt(Y[p][q]);
-        if constexpr (RB == 4) *reinterpret_cast<uint32_t*>(row) = pk.u[0];
-        if constexpr (RB == 8) *reinterpret_cast<uint2*>(row) = make_uint2(pk.u[0], pk.u[1]);
-        if constexpr (RB == 16) *reinterpret_cast<uint4*>(row) = make_uint4(pk.u[0], pk.u[1], pk.u[2], pk.u[3]);
-        continue;
+    store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
+  }
+}
+
+// TMA-staged K4 for large domains (D >= 7): a thread per (t, k) cannot keep
+// enough of its D^2 loads in flight, so M is streamed through shared memory
+// instead.  CTA = (128-tile block, 32 output channels); one producer thread
+// loads, per channel k, the piece {128 t, 1 k, Q points} of M (Q x 512 B) into
+// a ring of NB buffers (mbarriers), four warps (thread = tile) apply
+// Y = A^T M A to it in the same fp32 order as output_transform_nchw.
+template <int DT, int M, int D>
+__global__ void __launch_bounds__(160) output_transform_tma(const __grid_constant__ CUtensorMap tmMl, int K, int Ho,
+                                                            int Wo, int th, int tw, int T, int NB,
+                                                            const __grid_constant__ XformParams xp,
+                                                            typename DType<DT>::T* __restrict__ y) {
+  using Tr = DType<DT>;
+  using TT = typename Tr::T;
+  constexpr int Q = D * D;
+  extern __shared__ __align__(16) uint8_t k4t_smem_raw[];
+  uint8_t* sm = k4t_smem_raw + ((128u - (smem_u32(k4t_smem_raw) & 127u)) & 127u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm);
+  uint64_t* empty = full + NB;
+  float* buf = reinterpret_cast<float*>(sm + 128);
+  const int mb = blockIdx.x, k0 = blockIdx.y * 32, nk = min(K, k0 + 32) - k0;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int b = 0; b < NB; ++b) mbar_init(&full[b], 1), mbar_init(&empty[b], 128);
+    fence_barrier_init();
+    tma_prefetch(&tmMl);
+  }
+  __syncthreads();
+  if (tid >= 128) {   // producer warp
+    if (tid == 128) {
+      for (int j = 0; j < nk; ++j) {
+        const int b = j % NB;
+        if (j >= NB) mbar_wait(&empty[b], (uint32_t)(((j / NB) - 1) & 1));
+        mbar_arrive_expect_tx(&full[b], Q * 128 * 4);
+        tma_load_3d(buf + (size_t)b * Q * 128, &tmMl, &full[b], mb * 128, k0 + j, 0);
       }
     }
+    return;
+  }
+  const int t = mb * 128 + tid;
+  const int tj = t % tw, rest = t / tw, ti = rest % th, n = rest / th;
+  for (int j = 0; j < nk; ++j) {
+    const int b = j % NB;
+    mbar_wait(&full[b], (uint32_t)((j / NB) & 1));
+    if (t < T) {
+      const float* fb = buf + (size_t)b * Q * 128 + tid;
+      float Y[M][M];
 #pragma unroll
-    for (int q = 0; q < M; ++q)
-      if (tj * M + q < Wo) row[q] = Tr::cvt(Y[p][q]);
+      for (int p = 0; p < M; ++p)
+#pragma unroll
+        for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        float Mi[D];
+#pragma unroll
+        for (int jj = 0; jj < D; ++jj) Mi[jj] = fb[(i * D + jj) * 128];
+        float Z[M];
+#pragma unroll
+        for (int q = 0; q < M; ++q) {
+          float acc = 0.f;
+#pragma unroll
+          for (int jj = 0; jj < D; ++jj) acc = fmaf(Mi[jj], xp.AT[q][jj], acc);
+          Z[q] = acc;
+        }
+#pragma unroll
+        for (int p = 0; p < M; ++p)
+#pragma unroll
+          for (int q = 0; q < M; ++q) Y[p][q] = fmaf(xp.AT[p][i], Z[q], Y[p][q]);
+      }
+      TT* dst = y + (((size_t)n * K + k0 + j) * Ho + (size_t)ti * M) * Wo + (size_t)tj * M;
+#pragma unroll
+      for (int p = 0; p < M; ++p) {
+        if (ti * M + p >= Ho) break;
+        store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
+      }
+    }
+    mbar_arrive(&empty[b]);
   }
 }
 
@@ -1112,6 +1169,24 @@ static void launch_out(const OutArgs& a) {
     dim3 grid((a.T + 31) / 32, (a.K + KB - 1) / KB);
     kern<<<grid, 256, smem, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
     return;
+  }
+  if constexpr (D >= 7) {
+    constexpr int Q = D * D;
+    int NB = (int)((96 * 1024) / ((size_t)Q * 128 * 4));
+    NB = NB > 4 ? 4 : NB;
+    CUtensorMap tml;
+    const uint64_t dims[3] = {(uint64_t)a.Tp, (uint64_t)a.K, (uint64_t)Q};
+    const uint64_t str[2] = {(uint64_t)a.Tp * 4, (uint64_t)a.K * a.Tp * 4};
+    const uint32_t box[3] = {128, 1, (uint32_t)Q};
+    if (NB >= 2 && (reinterpret_cast<uintptr_t>(a.Mw) % 16) == 0 &&
+        make_map(&tml, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.Mw, dims, str, box, false)) {
+      const size_t smem = 256 + (size_t)NB * Q * 128 * 4;
+      auto kern = output_transform_tma<DT, M, D>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      dim3 grid((a.T + 127) / 128, (a.K + 31) / 32);
+      kern<<<grid, 160, smem, a.st>>>(tml, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, NB, *a.xp, (typename Tr::T*)a.y);
+      return;
+    }
   }
   dim3 grid((a.T + 127) / 128, a.K);
   output_transform_nchw<DT, M, D><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp,
