@@ -188,7 +188,8 @@ __device__ __forceinline__ void stage_halo(const typename Tr::T* xa, const typen
 }
 
 __host__ __device__ constexpr int k1_nchunk(int NX, int D) { return D * NX <= 36 ? 1 : (D * NX + 31) / 32; }
-__host__ __device__ constexpr int k1_jc(int NX, int D) { return (D + k1_nchunk(NX, D) - 1) / k1_nchunk(NX, D); }
+// larger tiles: two output columns per pass (measured best, scripts/ubench_k1rolled.cu)
+__host__ __device__ constexpr int k1_jc(int NX, int D) { return k1_nchunk(NX, D) == 1 ? D : 2; }
 
 // V = B^T d B for one tile and the channel pair of this lane.  The halo row a
 // (a < NX) of the tile starts at ring + slot(a) * SEG * 32 + col * 32, slot(a)
@@ -360,14 +361,16 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 #pragma unroll
       for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
   } else {
-#pragma unroll 1
-    for (int j0 = 0; j0 < D; j0 += JC) {
+    // JC output columns per pass; small enough domains unroll every pass
+    // (compile-time coefficient indices) with a memory clobber between passes
+    // so the scheduler cannot interleave them, larger ones roll the passes.
+    auto pass = [&](int j0) {
       float2 acc[D][JC];
 #pragma unroll
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int jj = 0; jj < JC; ++jj) acc[i][jj] = make_float2(0.f, 0.f);
-#pragma unroll 1
+#pragma unroll
       for (int a = 0; a < NX; ++a) {
         const int sa = s0 + a < RR ? s0 + a : s0 + a - RR;
         const PT* sd = ring + sa * 32 * SEGP + col;
@@ -394,6 +397,16 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 #pragma unroll
         for (int jj = 0; jj < JC; ++jj)
           if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+    };
+    if constexpr (NX * D <= 64) {
+#pragma unroll
+      for (int j0 = 0; j0 < D; j0 += JC) {
+        pass(j0);
+        asm volatile("" ::: "memory");
+      }
+    } else {
+#pragma unroll 1
+      for (int j0 = 0; j0 < D; j0 += JC) pass(j0);
     }
   }
 }
@@ -411,7 +424,7 @@ struct K1Geo {
 };
 
 template <int DT, int M, int NX, int D>
-__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), 2) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_nchunk(NX, D) == 1 ? 2 : 1) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
                                                               const __grid_constant__ K1Geo gk,
                                                               const __grid_constant__ XformParams xp,
                                                               typename DType<DT>::T* __restrict__ V, size_t qstride,
@@ -618,14 +631,16 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
 #pragma unroll
       for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
   } else {
-#pragma unroll 1
-    for (int j0 = 0; j0 < D; j0 += JC) {
+    // JC output columns per pass; small enough domains unroll every pass
+    // (compile-time coefficient indices) with a memory clobber between passes
+    // so the scheduler cannot interleave them, larger ones roll the passes.
+    auto pass = [&](int j0) {
       float2 acc[D][JC];
 #pragma unroll
       for (int i = 0; i < D; ++i)
 #pragma unroll
         for (int jj = 0; jj < JC; ++jj) acc[i][jj] = make_float2(0.f, 0.f);
-#pragma unroll 1
+#pragma unroll
       for (int a = 0; a < NX; ++a) {
         float2 d[NX];
         load_row(a, d);
@@ -649,6 +664,16 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
 #pragma unroll
         for (int jj = 0; jj < JC; ++jj)
           if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
+    };
+    if constexpr (NX * D <= 64) {
+#pragma unroll
+      for (int j0 = 0; j0 < D; j0 += JC) {
+        pass(j0);
+        asm volatile("" ::: "memory");
+      }
+    } else {
+#pragma unroll 1
+      for (int j0 = 0; j0 < D; j0 += JC) pass(j0);
     }
   }
 }
