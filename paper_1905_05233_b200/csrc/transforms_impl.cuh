@@ -414,7 +414,8 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 constexpr int K1_CONV_WARPS = 4;   // converter warps of input_transform_tma
 // compute warps per CTA: 7 for the fully unrolled small tiles, 5 for the rolled
 // larger ones (keeps two CTAs per SM with room for their registers)
-__host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_nchunk(NX, D) == 1 ? 7 : 5; }
+__host__ __device__ constexpr bool k1_small(int NX, int D) { return NX * D <= 36; }
+__host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_small(NX, D) ? 7 : 5; }
 
 struct K1Geo {
   int C, H, W, pad, th, tw, Cp, TJB;
@@ -424,7 +425,7 @@ struct K1Geo {
 };
 
 template <int DT, int M, int NX, int D>
-__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_nchunk(NX, D) == 1 ? 2 : 1) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
+__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_small(NX, D) ? 2 : 1) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
                                                               const __grid_constant__ K1Geo gk,
                                                               const __grid_constant__ XformParams xp,
                                                               typename DType<DT>::T* __restrict__ V, size_t qstride,
