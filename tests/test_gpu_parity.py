@@ -519,3 +519,23 @@ def test_host_io_chunked_equals_device_call(N, layout):
     W.wino_conv2d_host_io(xh, x2, wd, a, y2, yh, ws, layout=layout)
     torch.cuda.synchronize()
     assert torch.equal(yh, y_dev.cpu())
+
+
+def test_error_study_trends_on_gpu():
+    """Sec. 3.1 / Figure 1 on the GPU path (scripts/error_study.py,
+    1000 paired random tiles): fp32 error of the Toom-Cook sets grows with the
+    tile size in 1D and 2D, and at the 2D ratio 2.25 the a^2+1 set
+    W F(6x6) beats TC F(4x4) -- the same qualitative facts the
+    oracle's trend tests pin."""
+    import importlib.util
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("error_study", os.path.join(root, "scripts", "error_study.py"))
+    es = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(es)
+    rows = es.run(1000, dtypes=("fp32",), ns=(2, 4, 6, 8))
+    err = {(r["dim"], r["family"], r["n"]): r["mean_euclid"] for r in rows}
+    for dim in (1, 2):
+        lin = [err[(dim, "lin", n)] for n in (2, 4, 6, 8)]
+        assert all(a < b for a, b in zip(lin, lin[1:])), (dim, lin)
+    assert err[(2, "sup1[a^2+1]", 6)] < err[(2, "lin", 4)]
