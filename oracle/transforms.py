@@ -361,6 +361,45 @@ def make_transforms(moduli, n_o, n_h=3, sub_points=None):
     return ts
 
 
+# --------------------------------------------------------------------------- scaled transforms
+
+
+def _pow2_floor_log2(r):
+    """e with 2^e <= r < 2^(e+1) for a positive Fraction r (exact)."""
+    r = Fraction(r)
+    e = r.numerator.bit_length() - r.denominator.bit_length()
+    while Fraction(2) ** e > r:
+        e -= 1
+    while Fraction(2) ** (e + 1) <= r:
+        e += 1
+    return e
+
+
+def scale_pow2_balance(ts):
+    """Power-of-two diagonal rescaling of the Winograd points (the "scaled G and
+    A^T" conditioning trick of [Vincent17] that P:607 lists as composable with
+    the method; reading S1).  Point i's input-transform row (column i
+    of B) is multiplied by 2^-s_i and its output-transform row (row i of A) by
+    2^s_i, with s_i = floor(floor(log2(max|B[:, i]| / max|A[i, :]|)) / 2), so the
+    two magnitudes meet halfway.  The product A^T[(G g) (.) (B^T d)] is unchanged
+    exactly (each Hadamard term gains 2^-s_i and loses it again), and powers of
+    two are exact in every floating-point format."""
+    mu = ts.mu
+    B = [list(r) for r in ts.B]
+    A = [list(r) for r in ts.A]
+    for i in range(mu):
+        bmax = max(abs(Fraction(B[j][i])) for j in range(len(B)))
+        amax = max(abs(Fraction(a)) for a in A[i])
+        if bmax == 0 or amax == 0:
+            continue
+        s = _pow2_floor_log2(bmax / amax) // 2
+        f = Fraction(2) ** s
+        for j in range(len(B)):
+            B[j][i] = Fraction(B[j][i]) / f
+        A[i] = [Fraction(a) * f for a in A[i]]
+    return TransformSet(list(ts.moduli), ts.n_o, ts.n_h, [list(r) for r in ts.G], B, A)
+
+
 # --------------------------------------------------------------------------- O6
 
 

@@ -83,6 +83,11 @@ class WinoAlgo:
         exact = [[Fraction(int(num[i * cols + j]), int(den[i * cols + j])) for j in range(cols)] for i in range(rows)]
         return exact, f32.reshape(rows, cols)
 
+    def scale(self, mode="pow2"):
+        """Power-of-two point balancing (wino_scale_transforms, [Vincent17] per P:607)."""
+        check(lib().wino_scale_transforms(self._h, {"none": 0, "pow2": 1}[mode]))
+        return self
+
     def unit_table(self):
         u = self.units
         out_pt, in_pt, nterm = (np.zeros(u, np.int32) for _ in range(3))

@@ -181,4 +181,55 @@ wino_status wino_algo_units(const wino_algo* al, int32_t* out_pt, int32_t* in_pt
 
 void wino_algo_destroy(wino_algo* al) { delete al; }
 
+// Power-of-two balancing of the Winograd points (include/wino.h, S1):
+// B column i *= 2^-s_i, A row i *= 2^s_i, s_i = floor(floor(log2(max|B[:,i]| /
+// max|A[i,:]|)) / 2).  Exact; re-lowers the fp32 kernel parameters.
+static int floor_log2(const Rat& r) {   // r > 0
+  int e = 0;
+  Rat two = Rat(2), half = Rat::make(1, 2), p = Rat(1);
+  auto lt = [](const Rat& a, const Rat& b) { return (a - b).n < 0; };
+  auto le = [&](const Rat& a, const Rat& b) { return !lt(b, a); };
+  while (lt(r, p)) p = p * half, --e;            // now p <= r (or it was already)
+  while (le(p * two, r)) p = p * two, ++e;       // now p <= r < 2p
+  return e;
+}
+
+wino_status wino_scale_transforms(wino_algo* al, int32_t mode) {
+  if (!al) return set_last_error("wino_scale_transforms: NULL algo"), WINO_E_ARG;
+  if (mode == WINO_SCALE_NONE) return WINO_OK;
+  if (mode != WINO_SCALE_POW2_BALANCE) return set_last_error("wino_scale_transforms: bad mode"), WINO_E_ARG;
+  if (al->lowering != WINO_LOWER_SUBSOLVER)
+    return set_last_error("wino_scale_transforms: the SUBSOLVER lowering only"), WINO_E_UNSUPPORTED;
+  if (al->scaled) return set_last_error("wino_scale_transforms: already scaled"), WINO_E_ARG;
+  try {
+    const int D = al->D;
+    for (int i = 0; i < D; ++i) {
+      Rat bmax(0), amax(0);
+      auto absr = [](const Rat& q) { return q.n < 0 ? -q : q; };
+      auto gt = [](const Rat& a, const Rat& b) { return (a - b).n > 0; };
+      for (size_t j = 0; j < al->B.size(); ++j)
+        if (gt(absr(al->B[j][i]), bmax)) bmax = absr(al->B[j][i]);
+      for (size_t k = 0; k < al->A[i].size(); ++k)
+        if (gt(absr(al->A[i][k]), amax)) amax = absr(al->A[i][k]);
+      if (bmax.is_zero() || amax.is_zero()) continue;
+      const int e = floor_log2(bmax / amax);
+      const int s = e >= 0 ? e / 2 : -((-e + 1) / 2);   // floor(e / 2)
+      Rat f(1);
+      for (int t = 0; t < (s < 0 ? -s : s); ++t) f = f * Rat(2);
+      if (s < 0) f = Rat(1) / f;
+      for (size_t j = 0; j < al->B.size(); ++j) al->B[j][i] = al->B[j][i] / f;
+      for (size_t k = 0; k < al->A[i].size(); ++k) al->A[i][k] = al->A[i][k] * f;
+    }
+    for (int i = 0; i < D; ++i) {
+      for (int j = 0; j < al->nx; ++j) al->xp.BT[i][j] = rat_to_f32(al->B[j][i]);
+      for (int j = 0; j < al->m; ++j) al->xp.AT[j][i] = rat_to_f32(al->A[i][j]);
+    }
+    al->scaled = true;
+  } catch (const std::exception& ex) {
+    set_last_error(std::string("wino_scale_transforms: ") + ex.what());
+    return WINO_E_RANGE;
+  }
+  return WINO_OK;
+}
+
 }  // extern "C"

@@ -144,3 +144,30 @@ def test_named_sets_match_oracle_canonical():
         spec, m = canonical_spec(name)
         mods, m2 = T.canonical(name)
         assert m == m2 and [str(x) for x in T.parse_moduli(spec)] == [str(x) for x in mods]
+
+
+@pytest.mark.parametrize("name", ["lin2", "lin4", "lin6", "lin8", "sup1_4", "sup1_6", "sup1_8", "sup2_6", "sup2_8"])
+def test_scaled_generator_matches_oracle(name):
+    """wino_scale_transforms (C++) and oracle.transforms.scale_pow2_balance
+    (Python) apply the same exact power-of-two balancing independently."""
+    from oracle.transforms import canonical, make_transforms, moduli_spec, scale_pow2_balance
+    mods, m = canonical(name)
+    a = W.WinoAlgo(moduli_spec(mods), m).scale("pow2")
+    tss = scale_pow2_balance(make_transforms(mods, m))
+    for which, ref in (("G", tss.G), ("B", tss.B), ("A", tss.A)):
+        exact, f32 = a.matrix(which)
+        assert exact == _fr(ref), which
+        assert np.array_equal(f32.view(np.uint32), P.lower_f32(ref).view(np.uint32)), which
+
+
+def test_scale_errors():
+    a = W.WinoAlgo("0,-1,1,inf", 2)
+    a.scale("none")
+    a.scale("pow2")
+    with pytest.raises(W.WinoError) as e:
+        a.scale("pow2")
+    assert e.value.status == 1
+    r = W.WinoAlgo("0,a^2+1,inf", 2, lowering="residue")
+    with pytest.raises(W.WinoError) as e:
+        r.scale("pow2")
+    assert e.value.status == 4

@@ -523,7 +523,7 @@ def test_host_io_chunked_equals_device_call(N, layout):
 
 def test_error_study_trends_on_gpu():
     """Sec. 3.1 / Figure 1 on the GPU path (scripts/error_study.py,
-    1000 paired random tiles): fp32 error of the Toom-Cook sets grows with the
+    5000 paired random tiles, as P:531): fp32 error of the Toom-Cook sets grows with the
     tile size in 1D and 2D, and at the 2D ratio 2.25 the a^2+1 set
     W F(6x6) beats TC F(4x4) -- the same qualitative facts the
     oracle's trend tests pin."""
@@ -533,9 +533,33 @@ def test_error_study_trends_on_gpu():
     spec = importlib.util.spec_from_file_location("error_study", os.path.join(root, "scripts", "error_study.py"))
     es = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(es)
-    rows = es.run(1000, dtypes=("fp32",), ns=(2, 4, 6, 8))
+    rows = es.run(5000, dtypes=("fp32",), ns=(2, 4, 6, 8))
     err = {(r["dim"], r["family"], r["n"]): r["mean_euclid"] for r in rows}
     for dim in (1, 2):
         lin = [err[(dim, "lin", n)] for n in (2, 4, 6, 8)]
         assert all(a < b for a, b in zip(lin, lin[1:])), (dim, lin)
     assert err[(2, "sup1[a^2+1]", 6)] < err[(2, "lin", 4)]
+
+
+@pytest.mark.parametrize("name,dtype", [("lin8", "fp16"), ("lin8", "bf16"), ("lin6", "fp16"), ("sup1_8", "fp16")])
+def test_layer_scaled_transforms(name, dtype):
+    """Power-of-two point balancing on the GPU path (wino_scale_transforms):
+    the layer matches the oracle's pipeline emulation of the *scaled* matrices
+    within +-10 %, and for fp16 Toom-Cook F(8x8) it removes the range collapse
+    of the unscaled algorithm."""
+    mods, m = T.canonical(name)
+    a = W.WinoAlgo(T.moduli_spec(mods), m).scale("pow2")
+    tss = T.scale_pow2_balance(T.make_transforms(mods, m))
+    x, w = datagen.layer(1, 64, 136, 26, 26, dtype, seed=21)
+    y = W.wino_conv2d(dev(x, dtype), dev(w, dtype), a)
+    torch.cuda.synchronize()
+    yref = CV.direct_conv2d_f64(x, w, 1)
+    sg = MT.summary(MT.stats8(host(y), yref, m))
+    so = MT.summary(MT.stats8(P.pipeline_conv2d(tss, x, w, dtype), yref, m))
+    assert sg["nonfinite"] == so["nonfinite"] == 0
+    assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
+    if name == "lin8" and dtype == "fp16":
+        y0 = W.wino_conv2d(dev(x, dtype), dev(w, dtype), algo_pair(name)[0])
+        torch.cuda.synchronize()
+        s0 = MT.summary(MT.stats8(host(y0), yref, m))
+        assert s0["mean_rel"] > 10 * sg["mean_rel"], (s0, sg)

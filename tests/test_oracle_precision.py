@@ -272,3 +272,23 @@ def test_paper_mode_1d_fp32_is_plain_fp32():
         p = [np.float32(a * b) for a, b in zip(u, v)]
         yy = [dot(AT[i], p) for i in range(4)]
         assert np.array_equal(np.array(yy, np.float32), y[t].astype(np.float32))
+
+
+def test_pow2_scaling_fixes_fp16_range_collapse():
+    """P:596 attributes the fp16 failure of large Toom-Cook tiles to range; the
+    power-of-two point balancing (reading S1) removes it: fp16 F(8x8) mean
+    relative error drops from O(10) to O(0.1), while bf16 (fp32 range) and
+    fp32 errors are unchanged (scaling by powers of two commutes with
+    rounding away from the range limits)."""
+    mods, m = T.canonical("lin8")
+    ts = T.make_transforms(mods, m)
+    tss = T.scale_pow2_balance(ts)
+    res = {}
+    for dt in ("fp16", "bf16"):
+        x, w = datagen.layer(1, 32, 8, 18, 18, dt, seed=1)
+        yref = CV.direct_conv2d_f64(x, w, 1)
+        e0 = MT.summary(MT.stats8(P.pipeline_conv2d(ts, x, w, dt), yref, m))["mean_rel"]
+        e1 = MT.summary(MT.stats8(P.pipeline_conv2d(tss, x, w, dt), yref, m))["mean_rel"]
+        res[dt] = (e0, e1)
+    assert res["fp16"][0] > 1.0 and res["fp16"][1] < 0.5, res
+    assert abs(res["bf16"][1] / res["bf16"][0] - 1) < 0.02, res

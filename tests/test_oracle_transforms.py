@@ -380,3 +380,28 @@ def test_parse_moduli():
     assert [str(m) for m in mods] == ["0", "-1", "1/2", "a^2+1", "-1", "inf"]
     assert T.parse_poly("a^2 - a + 1") == (Fr(1), Fr(-1), Fr(1))
     assert T.parse_poly("2*a^2-1/2") == (Fr(-1, 2), Fr(0), Fr(2))
+
+
+@pytest.mark.parametrize("name", ["lin8", "lin6", "sup1_6", "sup2_6"])
+def test_scaled_transforms_stay_exact(name):
+    """Power-of-two point balancing (reading S1, [Vincent17] per P:607):
+    the scaled algorithm still computes exact correlation (brute force on a
+    random rational tile), the factors are powers of two, and for the
+    Toom-Cook tiles the largest output weight shrinks (16384 -> 4 at m = 8)."""
+    from fractions import Fraction
+    import random
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    tss = T.scale_pow2_balance(ts)
+    rnd = random.Random(3)
+    g = [[Fraction(rnd.randint(-9, 9), rnd.randint(1, 4)) for _ in range(3)] for _ in range(3)]
+    d = [[Fraction(rnd.randint(-9, 9), rnd.randint(1, 4)) for _ in range(m + 2)] for _ in range(m + 2)]
+    assert CV.winograd_2d_exact(tss, g, d) == CV.direct_corr_2d(g, d)
+    for i in range(ts.mu):
+        ratios = {Fraction(tss.A[i][k]) / Fraction(ts.A[i][k]) for k in range(m) if ts.A[i][k] != 0}
+        assert len(ratios) == 1
+        f = ratios.pop()
+        assert f.numerator & (f.numerator - 1) == 0 and f.denominator & (f.denominator - 1) == 0
+    if name == "lin8":
+        assert max(abs(a) for r in ts.A for a in r) == 16384
+        assert max(abs(a) for r in tss.A for a in r) == 4
