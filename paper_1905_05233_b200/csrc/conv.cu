@@ -71,8 +71,23 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   void* U = base + g.offU;
   void* V = base + g.offV;
   float* M = reinterpret_cast<float*>(base + g.offM);
-  if ((s = run_weight_transform(w, K, C, al, dt, U, st)) != WINO_OK) return s;
+  // K2 (weights) and K1 (inputs) are independent: K2 runs on a library-owned
+  // side stream forked from and joined back into the caller's stream (events,
+  // so the pair stays CUDA-graph capturable), overlapping K1's start.
+  static thread_local cudaStream_t s_side = nullptr;
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (!s_side) {
+    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
+    WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  cudaStream_t s_w = s_side;
+  WINO_CUDA_CHECK(cudaEventRecord(ev_fork, st));
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(s_w, ev_fork, 0));
+  if ((s = run_weight_transform(w, K, C, al, dt, U, s_w)) != WINO_OK) return s;
+  WINO_CUDA_CHECK(cudaEventRecord(ev_join, s_w));
   if ((s = run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, st)) != WINO_OK) return s;
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev_join, 0));
   if (layout == WINO_NCHW && !fused_disabled()) {
     s = run_domain_gemm_fused(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
     if (s != WINO_E_UNSUPPORTED) return s;   // OK or a real failure
