@@ -216,7 +216,8 @@ struct FuseArgs {
   const float* M;       // the M workspace (for the L2 discards)
   int* done;            // [nMB] point-GEMM items stored, per tile block (zeroed before the launch)
   int* fixed;           // [nMB] fixup items finished, per tile block (zeroed before the launch)
-  int lag;              // the producer starts tile block mb only once block mb - lag is fully fixed up
+  int dbg;              // timing experiments only (WINO_FUSED_DBG): 1 no wait, 2 no fixup math, 4 no discard, 8 no fixup loads
+  int lag;              // work-list distance, in tile blocks, from a block's GEMM items to its fixups
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -271,36 +272,42 @@ __device__ __forceinline__ void fixup_point(const float* fb, const FuseArgs& fa,
   }
 }
 
-constexpr int kFuseStages = 3;   // GEMM stages of the fused kernel (room for the M pieces)
-template <int BN>
-using FusedCfg = GemmCfg<false, BN, kFuseStages, 2>;
-// shared memory of the fused kernel: GEMM stages + 2 epilogue boxes + barriers,
-// then two M pieces of Q x 128 fp32 (one channel of every point for a 128-tile block)
-template <int BN>
-constexpr int fused_smem(int Q) { return FusedCfg<BN>::SMEM + 128 + 2 * Q * kBM * 4; }
+// Time-multiplexed persistent K3 + K4.  One ordered work list holds the
+// point-GEMM items of each 128-tile block mb (Q * nNB of them) and, LAG blocks
+// later, the block's fixup items (mb, 32-channel slice ks).  CTA c runs list
+// positions c, c + G, ... in order.  GEMM items use the warp-specialised
+// tcgen05 pipeline (producer / MMA / epilogue, which publishes each stored
+// item on done[mb]); at a fixup item every warp of the CTA meets at a barrier
+// (so the GEMM pipeline is drained) and the whole CTA turns into an output
+// transform: the 192 KB of stage memory becomes a ring of NB M pieces
+// ({128 t, 1 k, Q points} TMA boxes read from L2), two 128-thread halves apply
+// Y = A^T M A to alternate channels, store y and discard the consumed M lines
+// from L2 -- so M is written to and read from L2 only.  A fixup waits only for
+// GEMM items earlier in the list, and all CTAs are resident (cooperative
+// launch), so the smallest pending list position always makes progress.
 
 template <int BN, int STAGES, int DT, int MO, int DO>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(256, 1)
     domain_gemm_fused_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                              const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmMl,
                              int T, int K, int Cp, int nMB, int nNB, int Q, int S, uint32_t idesc,
                              const __grid_constant__ GemmSched gs, const __grid_constant__ FuseArgs fa) {
   using Cfg = GemmCfg<false, BN, STAGES, 2>;
   extern __shared__ uint8_t smem_raw[];
-  // 1024-byte aligned for the 128-byte swizzle atoms; offsetting the shared array keeps
-  // a shared-space pointer (STS / LDS, no generic stores and CTA-wide MEMBARs)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* ffull = tempty + 2;    // [2] M piece landed (TMA)
-  uint64_t* fempty = ffull + 2;    // [2] M piece consumed (128 fixup threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fempty + 2);
-  float* fbuf = reinterpret_cast<float*>(smem + Cfg::SMEM - 1024 + 128);   // 2 x [Q][128] fp32
+  uint64_t* ffull = tempty + 2;   // [kMaxPieces] M piece landed (TMA)
+  constexpr int kMaxPieces = 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ffull + kMaxPieces);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const uint32_t piece_bytes = (uint32_t)fa.Q * kBM * 4;
+  int NB = (STAGES * Cfg::STAGE_BYTES) / (int)piece_bytes;   // M pieces that fit in the stage memory
+  NB = (NB > kMaxPieces ? kMaxPieces : NB) & ~1;              // even: buffer b belongs to half b & 1
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmV);
     tma_prefetch(&tmU);
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(384, 1)
     tma_prefetch(&tmMl);
     for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
     for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
-    for (int a = 0; a < 2; ++a) mbar_init(&ffull[a], 1), mbar_init(&fempty[a], kBM);
+    for (int b = 0; b < kMaxPieces; ++b) mbar_init(&ffull[b], 1);
     fence_barrier_init();
     fence_proxy_async_shared();
   }
@@ -318,165 +325,154 @@ __global__ void __launch_bounds__(384, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int nItems = Q * nMB * nNB;
   const int KB = Cp / Cfg::BK;
-  // item -> (mb slowest, then output point p, then nb)
-  auto decode = [&](int item, int& mb, int& p, int& nb) {
-    nb = item % nNB;
-    p = (item / nNB) % Q;
-    mb = item / (nNB * Q);
+  const int IP = Q * nNB, nKS = fa.nKS, SEC = IP + nKS;
+  const int L = fa.lag < nMB ? fa.lag : nMB;
+  const int A_end = L * IP, B_end = A_end + (nMB - L) * SEC, LEN = B_end + L * nKS;
+  // list position -> GEMM item (mb, p, nb) or fixup item (mb, ks)
+  auto decode = [&](int w, bool& isF, int& mb, int& p, int& nb, int& ks) {
+    int r;
+    if (w < A_end) {
+      isF = false, mb = w / IP, r = w % IP;
+    } else if (w < B_end) {
+      const int u = w - A_end, sct = u / SEC;
+      r = u % SEC;
+      if (r < IP) isF = false, mb = L + sct;
+      else isF = true, mb = sct, ks = r - IP;
+    } else {
+      const int u = w - B_end;
+      isF = true, mb = (nMB - L) + u / nKS, ks = u % nKS;
+    }
+    if (!isF) p = r / nNB, nb = r % nNB;
   };
 
-  if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
-        int mb, p, nb;
-        decode(item, mb, p, nb);
-        // backpressure: keep at most `lag` tile blocks of M in flight in L2
-        if (mb >= fa.lag)
-          while (ld_acquire(fa.fixed + mb - fa.lag) < fa.nKS) __nanosleep(128);
-        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
-          const int qi = gs.in_pt[pr], sl = gs.slab[pr];
-          for (int kb = 0; kb < KB; ++kb) {
-            mbar_wait(&empty[stage], phase ^ 1);
-            mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-            uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-            tma_load_3d(base, &tmV, &full[stage], 0, 0, (qi * nMB + mb) * KB + kb);   // blocked V: one 16 KB block
-            tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
-            if (++stage == STAGES) stage = 0, phase ^= 1;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
-        int mb, p, nb;
-        decode(item, mb, p, nb);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        int step = 0;
-        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
-          for (int kb = 0; kb < KB; ++kb, ++step) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-            const uint32_t b0 = a0 + Cfg::A_BYTES;
-#pragma unroll
-            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
-              const uint32_t koff = k * Cfg::UK * Cfg::ES;
-              mma_ss<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc, (step | k) != 0);
+  // role state carried across list positions
+  int pstage = 0, mstage = 0, acc_m = 0, acc_e = 0, chunk = 0;
+  uint32_t pphase = 0, mphase = 0, accph_m = 0, accph_e = 0;
+  int piece = 0;   // running M-piece counter (fixups)
+  const int wq = warp & 3;
+  const bool storer = (warp == 4 && lane == 0);
+
+  for (int w = blockIdx.x; w < LEN; w += gridDim.x) {
+    bool isF;
+    int mb, p = 0, nb = 0, ks = 0;
+    decode(w, isF, mb, p, nb, ks);
+    if (!isF) {
+      if (warp == 0) {
+        if (lane == 0) {
+          fence_proxy_async_shared();   // a fixup may have read the stage memory through the generic proxy
+          for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+            const int qi = gs.in_pt[pr], sl = gs.slab[pr];
+            for (int kb = 0; kb < KB; ++kb) {
+              mbar_wait(&empty[pstage], pphase ^ 1);
+              mbar_arrive_expect_tx(&full[pstage], Cfg::STAGE_BYTES);
+              uint8_t* base = smem + pstage * Cfg::STAGE_BYTES;
+              tma_load_3d(base, &tmV, &full[pstage], 0, 0, (qi * nMB + mb) * KB + kb);
+              tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[pstage], kb * Cfg::BK, nb * BN, sl);
+              if (++pstage == STAGES) pstage = 0, pphase ^= 1;
             }
-            mma_commit(&empty[stage]);
-            if (++stage == STAGES) stage = 0, phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
-        if (++acc == 2) acc = 0, acc_phase ^= 1;
-      }
-    }
-    __syncwarp();
-  } else if (warp >= 4 && warp < 8) {
-    // -------------------------------------------------- epilogue: TMEM -> SMEM -> TMA store, then publish
-    const int wq = warp & 3;
-    const bool storer = (warp == 4 && lane == 0);
-    int acc = 0, chunk = 0;
-    uint32_t acc_phase = 0;
-    for (int item = blockIdx.x; item < nItems; item += gridDim.x) {
-      int mb, p, nb;
-      decode(item, mb, p, nb);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-#pragma unroll 1
-      for (int j0 = 0; j0 < BN; j0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
-        if (j0 + 32 == BN) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
-        }
-        if (nb * BN + j0 >= K) continue;
-        float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
-        if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
-        named_bar_sync(1, 128);
+        __syncwarp();
+      } else if (warp == 1) {
+        if (lane == 0) {
+          mbar_wait(&tempty[acc_m], accph_m ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc_m * BN;
+          int step = 0;
+          for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+            for (int kb = 0; kb < KB; ++kb, ++step) {
+              mbar_wait(&full[mstage], mphase);
+              tc_fence_after();
+              const uint32_t a0 = smem_u32(smem + mstage * Cfg::STAGE_BYTES);
+              const uint32_t b0 = a0 + Cfg::A_BYTES;
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
-        fence_proxy_async_shared();
-        named_bar_sync(1, 128);
+              for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+                const uint32_t koff = k * Cfg::UK * Cfg::ES;
+                mma_ss<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc, (step | k) != 0);
+              }
+              mma_commit(&empty[mstage]);
+              if (++mstage == STAGES) mstage = 0, mphase ^= 1;
+            }
+          }
+          mma_commit(&tfull[acc_m]);
+          if (++acc_m == 2) acc_m = 0, accph_m ^= 1;
+        }
+        __syncwarp();
+      } else if (warp >= 4) {
+        mbar_wait(&tfull[acc_e], accph_e);
+        tc_fence_after();
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc_e * BN + j0, v);
+          if (j0 + 32 == BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc_e]);
+          }
+          if (nb * BN + j0 >= K) continue;
+          float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
+          if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
+          fence_proxy_async_shared();
+          named_bar_sync(1, 128);
+          if (storer) {
+            tma_store_3d(&tmM, buf, mb * kBM, nb * BN + j0, p);
+            bulk_commit();
+          }
+          ++chunk;
+        }
+        if (++acc_e == 2) acc_e = 0, accph_e ^= 1;
         if (storer) {
-          tma_store_3d(&tmM, buf, mb * kBM, nb * BN + j0, p);
-          bulk_commit();
+          bulk_wait_all();   // the item's M boxes are in memory: publish them
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          red_release_add(fa.done + mb, 1);
         }
-        ++chunk;
       }
-      if (++acc == 2) acc = 0, acc_phase ^= 1;
-      if (storer) {
-        // the item's M boxes are in memory: publish them to the fixup warps
-        bulk_wait_all();
+    } else {
+      // ---------------------------------------------------------------- fixup item
+      __syncthreads();   // every warp is past its earlier items: the stage memory is free
+      if (tid == 0) {
+        if (!(fa.dbg & 1))
+          while (ld_acquire(fa.done + mb) < fa.need) __nanosleep(128);
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __threadfence();
-        red_release_add(fa.done + mb, 1);
+        fence_proxy_async_shared();
       }
-    }
-    if (storer) bulk_wait_all();
-  } else if (warp >= 8) {
-    // -------------------------------------------------- fixup warps: output transform from L2
-    // Fixup item (mb, ks): channels [32 ks, 32 ks + 32) of tile block mb.  One
-    // thread streams the item's M pieces (all Q points of one channel k, 128
-    // tiles: a {128, 1, Q} TMA box of M) through two shared-memory buffers;
-    // thread tl computes tile mb*128 + tl.  Consumed M lines are discarded
-    // from L2 (no write-back), and the block's `fixed` counter releases the
-    // producer's backpressure.
-    const int tl = threadIdx.x - 256;
-    const bool issuer = tl == 0;
-    const int nFix = nMB * fa.nKS;
-    const uint32_t piece_bytes = (uint32_t)fa.Q * kBM * 4;
-    const size_t qs = (size_t)fa.K * fa.Tp;
-    int piece = 0;   // running piece counter (buffer = piece & 1, use = piece >> 1)
-    for (int f = blockIdx.x; f < nFix; f += gridDim.x) {
-      const int mb = f / fa.nKS, ks = f % fa.nKS;
+      __syncthreads();
       const int k0 = ks * 32, nk = min(fa.K, k0 + 32) - k0;
-      if (issuer) {
-        while (ld_acquire(fa.done + mb) < fa.need) __nanosleep(256);
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        for (int j = 0; j < 2 && j < nk; ++j) {
-          const int pc = piece + j, b = pc & 1;
-          if (pc >= 2) mbar_wait(&fempty[b], (uint32_t)(((pc >> 1) - 1) & 1));
+      const int half = tid >> 7, tl = tid & (kBM - 1);
+      float* ring = reinterpret_cast<float*>(smem);
+      const size_t qs = (size_t)fa.K * fa.Tp;
+      // each half's thread 0 streams the pieces of its channels j = half, half + 2, ...
+      if (tl == 0 && !(fa.dbg & 8))
+        for (int j = half, n = 0; j < nk && n < NB / 2; j += 2, ++n) {
+          const int pc = piece + j, b = pc % NB;
           mbar_arrive_expect_tx(&ffull[b], piece_bytes);
-          tma_load_3d(fbuf + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + j, 0);
+          tma_load_3d(ring + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + j, 0);
         }
-      }
-      for (int j = 0; j < nk; ++j, ++piece) {
-        const int b = piece & 1;
-        mbar_wait(&ffull[b], (uint32_t)((piece >> 1) & 1));
-        const float* fb = fbuf + (size_t)b * fa.Q * kBM;
-        // the piece is in shared memory: its L2 lines (Q rows x 512 B) can go
-        for (int l = tl; l < fa.Q * 4; l += kBM)
-          discard_l2(fa.M + (size_t)(l >> 2) * qs + (size_t)(k0 + j) * fa.Tp + (size_t)mb * kBM + (l & 3) * 32);
+      for (int j = half; j < nk; j += 2) {
+        const int pc = piece + j, b = pc % NB;
+        if (!(fa.dbg & 8)) mbar_wait(&ffull[b], (uint32_t)((pc / NB) & 1));
+        const float* fb = ring + (size_t)b * fa.Q * kBM;
+        for (int l = tl; l < fa.Q * 4; l += kBM)   // lines past Tp belong to the next channel's row: keep them
+          if (mb * kBM + (l & 3) * 32 < fa.Tp && !(fa.dbg & 4))
+            discard_l2(fa.M + (size_t)(l >> 2) * qs + (size_t)(k0 + j) * fa.Tp + (size_t)mb * kBM + (l & 3) * 32);
         const int t = mb * kBM + tl;
-        if (t < fa.T) fixup_point<DT, MO, DO>(fb, fa, t, tl, k0 + j);
-        mbar_arrive(&fempty[b]);
-        if (issuer && j + 2 < nk) {
-          const int pc = piece + 2;
-          mbar_wait(&fempty[b], (uint32_t)(((pc >> 1) - 1) & 1));
+        if (t < fa.T && !(fa.dbg & 2)) fixup_point<DT, MO, DO>(fb, fa, t, tl, k0 + j);
+        named_bar_sync(2 + half, kBM);   // this half is done with buffer b
+        const int jn = j + NB;            // the next piece of this half that maps to buffer b
+        if (tl == 0 && jn < nk && !(fa.dbg & 8)) {
+          fence_proxy_async_shared();
           mbar_arrive_expect_tx(&ffull[b], piece_bytes);
-          tma_load_3d(fbuf + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + j + 2, 0);
+          tma_load_3d(ring + (size_t)b * fa.Q * kBM, &tmMl, &ffull[b], mb * kBM, k0 + jn, 0);
         }
       }
-      named_bar_sync(2, kBM);
-      if (issuer) {
-        __threadfence();
-        red_release_add(fa.fixed + mb, 1);
-      }
+      piece += nk;
+      __syncthreads();   // fixup done: the stage memory goes back to the GEMM
     }
   }
   __syncthreads();
@@ -521,9 +517,9 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
 template <int DT, int MO, int DO>
 static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
                                 const wino_algo* al, uint32_t fmt, const float* M, void* y, int* done, cudaStream_t st) {
-  constexpr int BN = 256, STAGES = kFuseStages;
+  constexpr int BN = 256, STAGES = 4;
   auto kern = domain_gemm_fused_kernel<BN, STAGES, DT, MO, DO>;
-  const int smem = fused_smem<BN>(g.Q);
+  const int smem = GemmCfg<false, BN, STAGES, 2>::SMEM;
   WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
   // M pieces for the fixup warps: box {128 t, 1 k, Q points} of M [Q][K][Tp]
@@ -544,11 +540,10 @@ static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, co
   fa.tw = g.tw, fa.nKS = (g.K + 31) / 32, fa.need = al->gs.Q * nNB, fa.y = y, fa.M = M, fa.done = done;
   fa.fixed = done + nMB;
   {
-    // tile blocks of M (Q * K * 128 * 4 bytes each) allowed in flight
-    const size_t blk = (size_t)g.Q * g.K * kBM * 4;
-    int lag = (int)((40u << 20) / (blk ? blk : 1));
-    fa.lag = lag < 2 ? 2 : lag;
-    if (const char* e = getenv("WINO_FUSED_LAG")) fa.lag = atoi(e);
+    // list distance (in tile blocks) between a block's GEMM items and its fixups
+    fa.lag = 2;
+    if (const char* e = getenv("WINO_FUSED_LAG")) fa.lag = atoi(e) < 1 ? 1 : atoi(e);
+    if (const char* e = getenv("WINO_FUSED_DBG")) fa.dbg = atoi(e);
   }
   WINO_CUDA_CHECK(cudaMemsetAsync(done, 0, sizeof(int) * 2 * nMB, st));
   const int items = al->gs.Q * nMB * nNB;
@@ -560,7 +555,7 @@ static wino_status launch_fused(const CUtensorMap& tv, const CUtensorMap& tu, co
   void* args[] = {(void*)&tv, (void*)&tu, (void*)&tm, (void*)&tml, &T, &K, &Cp, (void*)&nMBv, (void*)&nNBv, &Q, &S,
                   (void*)&idesc, (void*)&al->gs, (void*)&fa};
   // cooperative launch: every CTA is resident (the fixup warps wait on other CTAs' items)
-  WINO_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(384), args, smem, st));
+  WINO_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(256), args, smem, st));
   WINO_LAUNCH_CHECK();
   return WINO_OK;
 }
@@ -595,7 +590,7 @@ wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, co
                                   float* M, void* y, int* done, cudaStream_t st) {
   const int doff = al->D - al->m - 2;
   if (dt == WINO_F32 || g.K <= 128 || al->m < 2 || al->m > 8 || doff < 0 || doff > 2) return WINO_E_UNSUPPORTED;
-  if (fused_smem<256>(g.Q) > 227 * 1024) return WINO_E_UNSUPPORTED;   // the M pieces must fit (Q <= 49)
+  if ((4 * GemmCfg<false, 256, 4>::STAGE_BYTES) / (g.Q * kBM * 4) < 2) return WINO_E_UNSUPPORTED;   // >= 2 M pieces
   CUtensorMapDataType cdt = dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   constexpr int BN = 256;
   const uint32_t BK = 128 / (uint32_t)g.es;
