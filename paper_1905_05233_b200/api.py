@@ -177,10 +177,10 @@ def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
 
 
 def v_to_dense(V, T):
-    """Blocked V [planes][Q][TB][Cp/CBW][128][CBW] (include/wino.h) -> dense
+    """Blocked V [planes][TB][Cp/CBW][Q][128][CBW] (include/wino.h) -> dense
     [planes][Q][T][Cp] view for inspection (a copy)."""
-    P_, Q, TB, CB, _, CBW = V.shape
-    return V.permute(0, 1, 2, 4, 3, 5).reshape(P_, Q, TB * 128, CB * CBW)[:, :, :T]
+    P_, TB, CB, Q, _, CBW = V.shape
+    return V.permute(0, 3, 1, 4, 2, 5).reshape(P_, Q, TB * 128, CB * CBW)[:, :, :T]
 
 
 def v_from_dense(Vd):
@@ -190,7 +190,7 @@ def v_from_dense(Vd):
     TB = -(-T // 128)
     pad = torch.zeros((P_, Q, TB * 128, Cp), dtype=Vd.dtype, device=Vd.device)
     pad[:, :, :T] = Vd
-    return pad.reshape(P_, Q, TB, 128, Cp // CBW, CBW).permute(0, 1, 2, 4, 3, 5).contiguous()
+    return pad.reshape(P_, Q, TB, 128, Cp // CBW, CBW).permute(0, 2, 4, 1, 3, 5).contiguous()
 
 
 def wino_weight_transform(w, algo, stream=None):
@@ -204,7 +204,7 @@ def wino_weight_transform(w, algo, stream=None):
 
 
 def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
-    """V [planes][Q][TB][Cp/CBW][128][CBW] (blocked, see v_to_dense) in the storage
+    """V [planes][TB][Cp/CBW][Q][128][CBW] (blocked, see v_to_dense) in the storage
     dtype; x [N,C,H,W] or [N,H,W,C] ("nhwc")."""
     if layout == "nchw":
         N, C, H, W = x.shape
@@ -212,7 +212,7 @@ def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
         N, H, W, C = x.shape
     dt = _TORCH_DT[x.dtype]
     g = geometry(algo, N, C, H, W, 1, pad, dt)
-    V = torch.empty((g["planes"], g["Q"], g["TB"], g["Cp"] // g["CBW"], 128, g["CBW"]), dtype=x.dtype,
+    V = torch.empty((g["planes"], g["TB"], g["Cp"] // g["CBW"], g["Q"], 128, g["CBW"]), dtype=x.dtype,
                     device=x.device)
     check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
                                      _ptr(V), _stream(stream)))

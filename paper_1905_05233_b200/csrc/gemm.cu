@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-            tma_load_3d(base, &tmV, &full[stage], 0, 0, (qi * nMB + mb) * KB + kb);   // blocked V: one 16 KB block
+            tma_load_3d(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi);   // blocked V: one 16 KB block
             if constexpr (kTF32)
-              tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], 0, 0, ((qi + Q) * nMB + mb) * KB + kb);
+              tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], 0, 0, ((nMB + mb) * KB + kb) * Q + qi);
             uint8_t* bb = base + Cfg::NPL * Cfg::A_BYTES;
             tma_load_3d(bb, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
             if constexpr (kTF32) tma_load_3d(bb + Cfg::B_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl + S);
@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(256, 1)
               mbar_wait(&empty[pstage], pphase ^ 1);
               mbar_arrive_expect_tx(&full[pstage], Cfg::STAGE_BYTES);
               uint8_t* base = smem + pstage * Cfg::STAGE_BYTES;
-              tma_load_3d(base, &tmV, &full[pstage], 0, 0, (qi * nMB + mb) * KB + kb);
+              tma_load_3d(base, &tmV, &full[pstage], 0, 0, (mb * KB + kb) * fa.Q + qi);
               tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[pstage], kb * Cfg::BK, nb * BN, sl);
               if (++pstage == STAGES) pstage = 0, pphase ^= 1;
             }

@@ -1,5 +1,5 @@
 // geometry.hpp -- layer geometry and workspace layout of wino_conv2d
-// (include/wino.h): U [S][K][Cp] | V [Q][TB][Cp/CBW][128][CBW] | M [Q][K][Tp] fp32 | group counters.
+// (include/wino.h): U [S][K][Cp] | V [TB][Cp/CBW][Q][128][CBW] | M [Q][K][Tp] fp32 | group counters.
 #pragma once
 #include <cstddef>
 
@@ -19,11 +19,14 @@ struct Geo {
 };
 
 // Tiling of PAPER.md P:498: overlapping (m+2)x(m+2) tiles at stride m.
-// Element offset of V_q[t][c] inside one point plane of the blocked layout:
-// 16 KB blocks [128 t][CBW c], block (t / 128, c / CBW) at ((t/128) * Cp/CBW + c/CBW),
-// so every GEMM A-operand box is one contiguous 16 KB run.
-__host__ __device__ inline size_t v_offset(int t, int c, int Cp, int CBW) {
-  return ((size_t)(t >> 7) * (Cp / CBW) + c / CBW) * (128 * CBW) + (size_t)(t & 127) * CBW + c % CBW;
+// Element offset of V_0[t][c] in the blocked layout: 16 KB blocks [128 t][CBW c]
+// (every GEMM A-operand box is one contiguous 16 KB run), block (t / 128, c / CBW,
+// point q) at ((t/128) * Cp/CBW + c/CBW) * Q + q -- the Q point blocks of one
+// (tile block, channel block) are adjacent, so point q of a tile is at the
+// compile-time distance q * kVPointStride elements from point 0.
+constexpr int kVPointBytes = 16384;   // one [128 t][CBW c] block
+__host__ __device__ inline size_t v_offset(int t, int c, int Cp, int CBW, int Q) {
+  return ((size_t)(t >> 7) * (Cp / CBW) + c / CBW) * Q * (128 * CBW) + (size_t)(t & 127) * CBW + c % CBW;
 }
 
 inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int pad, wino_dtype dt) {

@@ -86,8 +86,8 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
     return WINO_E_UNSUPPORTED;
   }
   Geo g = make_geo(al, N, C, H, W, 1, pad, dt);
-  const size_t qstride = (size_t)g.TB * 128 * g.Cp;   // blocked V: one point plane
-  InArgs a{x, C, H, W, pad, g.th, g.tw, g.Cp, N, (int)layout, &al->xp, V, qstride, (size_t)g.Q * qstride, st};
+  const size_t qstride = (size_t)128 * g.CBW;   // blocked V: adjacent point blocks (geometry.hpp)
+  InArgs a{x, C, H, W, pad, g.th, g.tw, g.Cp, N, (int)layout, &al->xp, V, qstride, (size_t)g.Q * g.TB * 128 * g.Cp, st};
   in_fn_(dt, al->m, al->D - al->m - 2)(a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;

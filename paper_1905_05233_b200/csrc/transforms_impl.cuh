@@ -8,6 +8,7 @@
 #include "device.cuh"
 #include "geometry.hpp"
 #include "tmap.hpp"
+#include "bt_masks.hpp"
 
 namespace wino {
 
@@ -56,6 +57,10 @@ __global__ void __launch_bounds__(128) weight_transform_kernel(const typename DT
   }
 }
 
+#ifndef K1_SKIP
+#define K1_SKIP 0   // timing experiments only (K1 NCHW): 1 skips the tile transforms, 2 the
+                    // conversions, 4 stores every tile to tile 0/1, 8 drops the bf16 V stores
+#endif
 template <int DT>
 __device__ __forceinline__ void store_pair(typename DType<DT>::T* dst, float2 v, size_t plane) {
   if constexpr (DT == WINO_F32) {
@@ -67,6 +72,9 @@ __device__ __forceinline__ void store_pair(typename DType<DT>::T* dst, float2 v,
   } else if constexpr (DT == WINO_F16) {
     *reinterpret_cast<__half2*>(dst) = __float22half2_rn(v);
   } else {
+#if defined(K1_SKIP) && (K1_SKIP & 8)
+    if (v.x == 1234.5f)   // timing experiment: keep the math, drop the stores
+#endif
     *reinterpret_cast<__nv_bfloat162*>(dst) = __float22bfloat162_rn(v);
   }
 }
@@ -109,6 +117,27 @@ __global__ void __launch_bounds__(128) weight_transform_points(const typename DT
     }
   }
 }
+
+// Zero patterns of B^T baked into K1 at compile time (bt_masks.hpp): DenseBT
+// keeps every term; MaskBT<w0, w1> has bit j * n_x + q set where B^T[j][q] != 0.
+// The transform loops are fully unrolled, so a false nz() removes the term's
+// FFMA2 (the coefficient values stay runtime kernel parameters).  Skipping a
+// zero term can only change the sign of an exact zero result.
+struct DenseBT {
+  __host__ __device__ static constexpr bool nz(int, int, int) { return true; }
+  __host__ __device__ static constexpr int first(int, int) { return 0; }
+};
+template <uint64_t W0, uint64_t W1>
+struct MaskBT {
+  __host__ __device__ static constexpr bool nz(int j, int q, int nx) {
+    return j * nx + q < 64 ? ((W0 >> (j * nx + q)) & 1) != 0 : ((W1 >> (j * nx + q - 64)) & 1) != 0;
+  }
+  __host__ __device__ static constexpr int first(int i, int nx) {   // first nonzero column of row i
+    int a = 0;
+    while (a < nx && !nz(i, a, nx)) ++a;
+    return a;
+  }
+};
 
 // ------------------------------------------------------------------ K1 input transform (NCHW)
 // Channel-pair design for sm_100a.  CTA = (tile-column block of TJB tiles,
@@ -326,7 +355,7 @@ template <> struct PairT<WINO_F16> {
   }
 };
 
-template <int DT, int NX, int D, typename PT>
+template <int DT, int NX, int D, typename PT, typename MK = DenseBT>
 __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int RR, int SEGP, int col,
                                                     const XformParams& xp, typename DType<DT>::T* out,
                                                     size_t qstride, size_t plane) {
@@ -334,6 +363,10 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
   constexpr int JC = k1_jc(NX, D);
   if constexpr (k1_nchunk(NX, D) == 1) {
     float2 acc[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[i][j] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int a = 0; a < NX; ++a) {
       const int sa = s0 + a < RR ? s0 + a : s0 + a - RR;
@@ -347,12 +380,14 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 #pragma unroll
         for (int q = 0; q < NX; ++q) {
           const float c = xp.BT[j][q];
-          rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+          if (MK::nz(j, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           const float c = xp.BT[i][a];
-          acc[i][j] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
+          if (MK::nz(i, a, NX))
+            acc[i][j] = a == MK::first(i, NX) ? __fmul2_rn(rt, make_float2(c, c))
+                                              : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
         }
       }
     }
@@ -383,12 +418,12 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 #pragma unroll
           for (int q = 0; q < NX; ++q) {
             const float c = xp.BT[j0 + jj < D ? j0 + jj : D - 1][q];
-            rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+            if (MK::nz(j0 + jj < D ? j0 + jj : D - 1, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
           }
 #pragma unroll
           for (int i = 0; i < D; ++i) {
             const float c = xp.BT[i][a];
-            acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+            if (MK::nz(i, a, NX)) acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
           }
         }
       }
@@ -411,7 +446,10 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
   }
 }
 
-constexpr int K1_CONV_WARPS = 4;   // converter warps of input_transform_tma
+#ifndef K1_CONV_WARPS_DEF
+#define K1_CONV_WARPS_DEF 4
+#endif
+constexpr int K1_CONV_WARPS = K1_CONV_WARPS_DEF;   // converter warps of input_transform_tma
 // compute warps per CTA: 7 for the fully unrolled small tiles, 5 for the rolled
 // larger ones (keeps two CTAs per SM with room for their registers)
 __host__ __device__ constexpr bool k1_small(int NX, int D) { return NX * D <= 36; }
@@ -424,7 +462,7 @@ struct K1Geo {
   unsigned box_bytes, slot_bytes;
 };
 
-template <int DT, int M, int NX, int D>
+template <int DT, int M, int NX, int D, typename MK = DenseBT>
 __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_small(NX, D) ? 2 : 1) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
                                                               const __grid_constant__ K1Geo gk,
                                                               const __grid_constant__ XformParams xp,
@@ -555,7 +593,9 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_sma
       __syncwarp();
       if (ti + 1 < th) {
         wait(ti + 1);
+#if !(K1_SKIP & 2)
         convert(ti + 1);
+#endif
       }
     } else {
       const int s0 = (ti * M - pad + 8 * RR) % RR;
@@ -563,8 +603,13 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_sma
         const int tj = tj0 + tjl;
         if (tj >= gk.tw) break;
         const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-        transform_tile_ring<DT, NX, D, PT>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(TT)),
-                                           qstride, plane);
+#if (K1_SKIP & 4)
+        transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)(t & 1), ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
+                                           kVPointBytes / sizeof(TT), plane);
+#elif !(K1_SKIP & 1)
+        transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
+                                           kVPointBytes / sizeof(TT), plane);
+#endif
       }
     }
     __syncthreads();
@@ -587,7 +632,7 @@ struct K1NGeo {
   unsigned box_bytes, slot_bytes;
 };
 
-template <int DT, int NX, int D, typename PT>
+template <int DT, int NX, int D, typename PT, typename MK = DenseBT>
 __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int rowoff, int colbase,
                                                    const XformParams& xp, typename DType<DT>::T* out,
                                                    size_t qstride, size_t plane) {
@@ -609,6 +654,10 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
   if constexpr (k1_nchunk(NX, D) == 1) {
     float2 acc[D][D];
 #pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
     for (int a = 0; a < NX; ++a) {
       float2 d[NX];
       load_row(a, d);
@@ -618,12 +667,14 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
 #pragma unroll
         for (int q = 0; q < NX; ++q) {
           const float c = xp.BT[j][q];
-          rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+          if (MK::nz(j, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
         }
 #pragma unroll
         for (int i = 0; i < D; ++i) {
           const float c = xp.BT[i][a];
-          acc[i][j] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
+          if (MK::nz(i, a, NX))
+            acc[i][j] = a == MK::first(i, NX) ? __fmul2_rn(rt, make_float2(c, c))
+                                              : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
         }
       }
     }
@@ -651,12 +702,12 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
 #pragma unroll
           for (int q = 0; q < NX; ++q) {
             const float c = xp.BT[j0 + jj < D ? j0 + jj : D - 1][q];
-            rt = __ffma2_rn(d[q], make_float2(c, c), rt);
+            if (MK::nz(j0 + jj < D ? j0 + jj : D - 1, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
           }
 #pragma unroll
           for (int i = 0; i < D; ++i) {
             const float c = xp.BT[i][a];
-            acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
+            if (MK::nz(i, a, NX)) acc[i][jj] = __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
           }
         }
       }
@@ -679,7 +730,7 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
   }
 }
 
-template <int DT, int M, int NX, int D>
+template <int DT, int M, int NX, int D, typename MK = DenseBT>
 __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_constant__ CUtensorMap tmx,
                                                                const __grid_constant__ K1NGeo gk,
                                                                const __grid_constant__ XformParams xp,
@@ -730,8 +781,8 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
       const int tj = tj0 + tjl;
       if (tj >= gk.tw) break;
       const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-      transform_tile_box<DT, NX, D, PT>(box, gk.BOXW, rowoff, tjl * M + col0 - cst, xp,
-                                        V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(typename DType<DT>::T)), qstride,
+      transform_tile_box<DT, NX, D, PT, MK>(box, gk.BOXW, rowoff, tjl * M + col0 - cst, xp,
+                                        V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(typename DType<DT>::T), D * D), kVPointBytes / sizeof(typename DType<DT>::T),
                                         plane);
     }
     __syncwarp();
@@ -773,7 +824,8 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
       rowT[a][j] = acc;
     }
   }
-  typename Tr::T* out = V + v_offset(t, ca, Cp, 128 / (int)sizeof(typename Tr::T));
+  typename Tr::T* out = V + v_offset(t, ca, Cp, 128 / (int)sizeof(typename Tr::T), D * D);
+  constexpr size_t qstride_c = kVPointBytes / sizeof(typename Tr::T);
 #pragma unroll
   for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -781,7 +833,7 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
       float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
       for (int a = 0; a < NX; ++a) acc = __ffma2_rn(rowT[a][j], make_float2(xp.BT[i][a], xp.BT[i][a]), acc);
-      store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc, plane);
+      store_pair<DT>(out + (size_t)(i * D + j) * qstride_c, acc, plane);
     }
 }
 
@@ -817,8 +869,8 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
     const int tj = tj0 + tjl;
     if (tj >= tw) break;
     const size_t t = ((size_t)n * th + ti) * tw + tj;
-    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + v_offset((int)t, ca, Cp, 128 / (int)sizeof(TT)),
-                                    qstride, plane);
+    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + v_offset((int)t, ca, Cp, 128 / (int)sizeof(TT), D * D),
+                                    kVPointBytes / sizeof(TT), plane);
   }
 }
 
@@ -1055,6 +1107,41 @@ struct OutArgs {
 using InFn = void (*)(const InArgs&);
 using OutFn = void (*)(const OutArgs&);
 
+// B^T zero pattern of the runtime algorithm (bit j * n_x + q, as in bt_masks.hpp)
+inline void bt_mask(const XformParams& xp, int nx, int D, uint64_t& w0, uint64_t& w1) {
+  w0 = w1 = 0;
+  for (int j = 0; j < D; ++j)
+    for (int q = 0; q < nx; ++q)
+      if (xp.BT[j][q] != 0.f) {
+        const int b = j * nx + q;
+        (b < 64 ? w0 : w1) |= 1ull << (b & 63);
+      }
+}
+// K1 kernel for the algorithm's zero pattern: a compiled zero-skipping instance
+// when the pattern is one of bt_masks.hpp, else the dense one
+template <int DT, int M, int NX, int D>
+static auto pick_k1_tma(const XformParams& xp) {
+  auto kern = input_transform_tma<DT, M, NX, D, DenseBT>;
+  uint64_t w0, w1;
+  bt_mask(xp, NX, D, w0, w1);
+#define WINO_PICK(nx_, d_, a_, b_) \
+  if constexpr (nx_ == NX && d_ == D) { if (w0 == a_ && w1 == b_) kern = input_transform_tma<DT, M, NX, D, MaskBT<a_, b_>>; }
+  WINO_BT_MASKS(WINO_PICK)
+#undef WINO_PICK
+  return kern;
+}
+template <int DT, int M, int NX, int D>
+static auto pick_k1_nhwc(const XformParams& xp) {
+  auto kern = input_transform_nhwc<DT, M, NX, D, DenseBT>;
+  uint64_t w0, w1;
+  bt_mask(xp, NX, D, w0, w1);
+#define WINO_PICK(nx_, d_, a_, b_) \
+  if constexpr (nx_ == NX && d_ == D) { if (w0 == a_ && w1 == b_) kern = input_transform_nhwc<DT, M, NX, D, MaskBT<a_, b_>>; }
+  WINO_BT_MASKS(WINO_PICK)
+#undef WINO_PICK
+  return kern;
+}
+
 template <int DT, int M, int D>
 static void launch_in_nhwc(const InArgs& a) {
   using TT = typename DType<DT>::T;
@@ -1082,7 +1169,7 @@ static void launch_in_nhwc(const InArgs& a) {
     ok = make_map(&tm, cdt, 4, a.x, dims, str, box, false);
   }
   if (ok) {
-    auto kern = input_transform_nhwc<DT, M, NX, D>;
+    auto kern = pick_k1_nhwc<DT, M, NX, D>(*a.xp);
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
     const int cw = gk.TJB < 7 ? gk.TJB : 7;   // compute warps (+1 TMA producer warp)
@@ -1159,7 +1246,7 @@ static void launch_in(const InArgs& a) {
     }
     ok = smem <= 200 * 1024;
     if (ok) {
-      auto kern = input_transform_tma<DT, M, NX, D>;
+      auto kern = pick_k1_tma<DT, M, NX, D>(*a.xp);
       if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       constexpr int MAXCW = k1_maxcw(NX, D);
       const int nthr = 32 * ((gk.TJB < MAXCW ? gk.TJB : MAXCW) + K1_CONV_WARPS);   // compute + converter warps
