@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(128) weight_transform_kernel(const typename DT
 
 #ifndef K1_SKIP
 #define K1_SKIP 0   // timing experiments only (K1 NCHW): 1 skips the tile transforms, 2 the
-                    // conversions, 4 stores every tile to tile 0/1, 8 drops the bf16 V stores
+                    // conversions, 8 drops the bf16 V stores
 #endif
 template <int DT>
 __device__ __forceinline__ void store_pair(typename DType<DT>::T* dst, float2 v, size_t plane) {
@@ -603,10 +603,7 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_sma
         const int tj = tj0 + tjl;
         if (tj >= gk.tw) break;
         const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-#if (K1_SKIP & 4)
-        transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)(t & 1), ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
-                                           kVPointBytes / sizeof(TT), plane);
-#elif !(K1_SKIP & 1)
+#if !(K1_SKIP & 1)
         transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
                                            kVPointBytes / sizeof(TT), plane);
 #endif
