@@ -33,9 +33,11 @@ INF = "inf"
 # "known good root points: 0, -1, 1, -1/2, 2, 1/2, -2, -1/4, 4".
 PAPER_POINTS = [Fraction(0), Fraction(-1), Fraction(1), Fraction(-1, 2), Fraction(2),
                 Fraction(1, 2), Fraction(-2), Fraction(-1, 4), Fraction(4)]
-# the same points reordered so the first five are BASELINE cfg3's set.
+# the same points reordered so the first five are BASELINE cfg3's set,
+# then 1/4, -4 (reading A21: P:533 lists nine points, Table 3's W(12x12)
+# takes TC(10x10)'s eleven; the list continues its +-2^k alternation).
 CANON_POINTS = [Fraction(0), Fraction(-1), Fraction(1), Fraction(-1, 2), Fraction(1, 2),
-                Fraction(2), Fraction(-2), Fraction(-1, 4), Fraction(4)]
+                Fraction(2), Fraction(-2), Fraction(-1, 4), Fraction(4), Fraction(1, 4), Fraction(-4)]
 # "To solve the subproblem ... we use F_TC(2x2, 2x2) and root points 0, -1 and inf".
 DEFAULT_SUB_POINTS = [Fraction(0), Fraction(-1), INF]
 

@@ -8,7 +8,7 @@ wino_make_transforms.  Points: PAPER.md P:533 ("0, -1, 1, -1/2, 2, 1/2, -2,
 """
 import re
 
-POINTS = ["0", "-1", "1", "-1/2", "1/2", "2", "-2", "-1/4", "4"]
+POINTS = ["0", "-1", "1", "-1/2", "1/2", "2", "-2", "-1/4", "4", "1/4", "-4"]   # + 1/4, -4: reading A21
 
 
 def canonical_spec(name):

@@ -11,8 +11,8 @@
 namespace wino {
 
 constexpr int kMaxDomain = 16;   // mu (or n_x) per dimension
-constexpr int kMaxNx = 10;       // m + 2, m <= 8
-constexpr int kMaxM = 8;
+constexpr int kMaxNx = 14;       // m + 2, m <= 12
+constexpr int kMaxM = 12;
 constexpr int kMaxUnits = 256;   // GEMM units per 2D tile
 
 struct Modulus {

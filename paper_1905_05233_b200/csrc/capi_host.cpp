@@ -90,8 +90,8 @@ wino_status wino_make_transforms(const wino_modulus* mods, int32_t n_mods, int32
     return WINO_E_ARG;
   }
   *out = nullptr;
-  if (r != 3 || m < 2 || m > 8) {
-    set_last_error("wino_make_transforms: only r = 3 and 2 <= m <= 8 are supported");
+  if (r != 3 || m < 2 || m > 12) {
+    set_last_error("wino_make_transforms: only r = 3 and 2 <= m <= 12 are supported");
     return WINO_E_UNSUPPORTED;
   }
   std::vector<Modulus> v(n_mods), sp(n_sub);

@@ -223,6 +223,7 @@ wino_status wino_conv1d_tiles(const void* x, const void* h, int64_t T, const win
   if (al->lowering != WINO_LOWER_SUBSOLVER) return set_last_error("1D tiles: SUBSOLVER algos only"), WINO_E_UNSUPPORTED;
   const int dm = al->mu - al->m - 2;
   if (dm < 0 || dm > 2) return set_last_error("1D tiles: mu must be in [m+2, m+4]"), WINO_E_UNSUPPORTED;
+  if (al->m > 8) return set_last_error("1D tiles: m <= 8 only"), WINO_E_UNSUPPORTED;
   if (T == 0) return WINO_OK;
   C1Args a{x, h, T, &al->xp, y, reinterpret_cast<cudaStream_t>(stream)};
   kC1[per_op_rounding ? 1 : 0][dt][al->m - 2][dm](a);

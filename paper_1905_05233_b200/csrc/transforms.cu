@@ -12,15 +12,19 @@
 namespace wino {
 
 static InFn in_fn_(int dt, int m, int doff) {
-  const InFn(*t)[3] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
+  const InFn(*t)[kTabD] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
   return t[m - 2][doff];
 }
 static OutFn out_fn_(int dt, int m, int doff) {
-  const OutFn(*t)[3] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
+  const OutFn(*t)[kTabD] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
   return t[m - 2][doff];
 }
 
-static bool md_ok(const wino_algo* al) { return al->m >= 2 && al->m <= 8 && al->D - al->m - 2 >= 0 && al->D - al->m - 2 <= 2; }
+// (m, D) with compiled transform kernels (WINO_TABLE)
+static bool md_ok(const wino_algo* al) {
+  const int doff = al->D - al->m - 2;
+  return al->m >= 2 && al->m <= 12 && doff >= 0 && doff < kTabD && in_fn_(WINO_BF16, al->m, doff) != nullptr;
+}
 
 template <int DT, int D>
 static void launch_wpts(const void* w, int K, int C, int Cp, const XformParams& xp, void* U, size_t plane,
@@ -42,6 +46,10 @@ static bool weight_points(int D, const void* w, int K, int C, int Cp, const Xfor
     case 10: launch_wpts<DT, 10>(w, K, C, Cp, xp, U, plane, st); return true;
     case 11: launch_wpts<DT, 11>(w, K, C, Cp, xp, U, plane, st); return true;
     case 12: launch_wpts<DT, 12>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 13: launch_wpts<DT, 13>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 14: launch_wpts<DT, 14>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 15: launch_wpts<DT, 15>(w, K, C, Cp, xp, U, plane, st); return true;
+    case 16: launch_wpts<DT, 16>(w, K, C, Cp, xp, U, plane, st); return true;
     default: return false;
   }
 }

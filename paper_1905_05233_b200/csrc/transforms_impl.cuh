@@ -1304,12 +1304,18 @@ static void launch_out(const OutArgs& a) {
 }
 
 // m in [2, 8], domain D in [m + 2, m + 4] (at most two quadratic moduli).
-#define WINO_ROW(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>}
-#define WINO_TABLE(F, DT) \
-  {WINO_ROW(F, DT, 2), WINO_ROW(F, DT, 3), WINO_ROW(F, DT, 4), WINO_ROW(F, DT, 5), WINO_ROW(F, DT, 6), WINO_ROW(F, DT, 7), WINO_ROW(F, DT, 8)}
+// [m - 2][D - m - 2]: m = 2..12, D = m + 2 .. m + 5 (each degree-d modulus adds
+// d - 1 domain points); the largest tiles (m >= 9) stop at D = m + 4.
+#define WINO_ROW(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>, &F<DT, M, M + 5>}
+#define WINO_ROW3(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>, nullptr}
+#define WINO_TABLE(F, DT)                                                                                         \
+  {WINO_ROW(F, DT, 2),  WINO_ROW(F, DT, 3),  WINO_ROW(F, DT, 4),  WINO_ROW(F, DT, 5),                            \
+   WINO_ROW(F, DT, 6),  WINO_ROW(F, DT, 7),  WINO_ROW(F, DT, 8),  WINO_ROW3(F, DT, 9),                           \
+   WINO_ROW3(F, DT, 10), WINO_ROW3(F, DT, 11), WINO_ROW3(F, DT, 12)}
+constexpr int kTabM = 11, kTabD = 4;
 
 // per-dtype tables (xform_<dt>.cu)
-extern const InFn kInTableF32[7][3], kInTableF16[7][3], kInTableBF16[7][3];
-extern const OutFn kOutTableF32[7][3], kOutTableF16[7][3], kOutTableBF16[7][3];
+extern const InFn kInTableF32[kTabM][kTabD], kInTableF16[kTabM][kTabD], kInTableBF16[kTabM][kTabD];
+extern const OutFn kOutTableF32[kTabM][kTabD], kOutTableF16[kTabM][kTabD], kOutTableBF16[kTabM][kTabD];
 
 }  // namespace wino

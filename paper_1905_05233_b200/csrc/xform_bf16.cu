@@ -2,6 +2,6 @@
 #include "transforms_impl.cuh"
 
 namespace wino {
-const InFn kInTableBF16[7][3] = WINO_TABLE(launch_in, WINO_BF16);
-const OutFn kOutTableBF16[7][3] = WINO_TABLE(launch_out, WINO_BF16);
+const InFn kInTableBF16[kTabM][kTabD] = WINO_TABLE(launch_in, WINO_BF16);
+const OutFn kOutTableBF16[kTabM][kTabD] = WINO_TABLE(launch_out, WINO_BF16);
 }  // namespace wino

@@ -2,6 +2,6 @@
 #include "transforms_impl.cuh"
 
 namespace wino {
-const InFn kInTableF16[7][3] = WINO_TABLE(launch_in, WINO_F16);
-const OutFn kOutTableF16[7][3] = WINO_TABLE(launch_out, WINO_F16);
+const InFn kInTableF16[kTabM][kTabD] = WINO_TABLE(launch_in, WINO_F16);
+const OutFn kOutTableF16[kTabM][kTabD] = WINO_TABLE(launch_out, WINO_F16);
 }  // namespace wino

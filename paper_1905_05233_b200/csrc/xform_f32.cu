@@ -2,6 +2,6 @@
 #include "transforms_impl.cuh"
 
 namespace wino {
-const InFn kInTableF32[7][3] = WINO_TABLE(launch_in, WINO_F32);
-const OutFn kOutTableF32[7][3] = WINO_TABLE(launch_out, WINO_F32);
+const InFn kInTableF32[kTabM][kTabD] = WINO_TABLE(launch_in, WINO_F32);
+const OutFn kOutTableF32[kTabM][kTabD] = WINO_TABLE(launch_out, WINO_F32);
 }  // namespace wino

@@ -1,0 +1,17 @@
+# round-end style validation + evidence refresh (one gpurun call); ncu reports are
+# exported to text on the box (the .ncu-rep files are too big to bring back)
+set -x
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_final.json 2> gpurun_out/bench_final.err
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+B="python bench.py --steps 3 --warmup 3 --no-extras"
+timeout 300 $B > gpurun_out/p_plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_r01b.csv $B > gpurun_out/ncu_launch.log 2>&1
+for k in input_transform domain_gemm output_transform weight_transform; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 -o /tmp/profb_$k $B > gpurun_out/ncub_$k.log 2>&1
+  ncu -i /tmp/profb_$k.ncu-rep --page raw --csv > gpurun_out/profb_$k.raw.csv 2>/dev/null
+  ncu -i /tmp/profb_$k.ncu-rep --page details > gpurun_out/profb_$k.details.txt 2>/dev/null
+  ncu -i /tmp/profb_$k.ncu-rep --page source --csv --print-source sass > gpurun_out/profb_$k.source.csv 2>/dev/null
+done
+ls -la gpurun_out/

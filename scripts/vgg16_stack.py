@@ -6,6 +6,13 @@ time (CUDA events, wino_conv2d incl. its weight transform) and the error vs the
 fp64 direct convolution on the device (on a 2-image sample, chained on the
 Winograd activations).  ReLU / max-pool between layers are torch glue, not timed.
 
+Network-level proxy for PAPER.md Tables 2-3 (real top-1 needs
+ImageNet and trained weights, out of scope): on the first --proxy images, the
+whole Winograd-chained stack + final max-pool feeds a random He-normal
+classifier (25088 -> 1000, fp64), and its argmax is compared with the same
+network run with fp64 direct convolutions (and, as a baseline for what any
+bf16 pipeline loses, with bf16 cuDNN direct convolutions).
+
     python scripts/vgg16_stack.py [--n 64] [--algos lin4,sup1_4,lin6,sup1_6] > profiles/vgg16_stack_r01.json
 """
 import argparse
@@ -26,6 +33,7 @@ def main():
     ap.add_argument("--algos", default="lin4,sup1_4,lin6,sup1_6")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--sample", type=int, default=2)
+    ap.add_argument("--proxy", type=int, default=32, help="images for the classifier-argmax proxy (0: off)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -44,6 +52,7 @@ def main():
     out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, bf16, "
                        f"error on {a.sample} images vs fp64 direct", "algos": {}}
     st = torch.cuda.current_stream()
+    finals = {}
     for name in a.algos.split(","):
         spec, m = canonical_spec(name)
         algo = Wn.WinoAlgo(spec, m)
@@ -78,8 +87,48 @@ def main():
             act = torch.relu(y)
             li += 1
         out["algos"][name] = {"spec": spec, "m": m, "mu": algo.mu, "layers": rows, "total_ms": total}
+        if a.proxy:
+            finals[name] = torch.nn.functional.max_pool2d(act[:a.proxy], 2).double().flatten(1)
         torch.cuda.empty_cache()
+    if a.proxy:
+        out["classifier_proxy"] = proxy(a, x0, weights, finals, rng)
     print(json.dumps(out, indent=1))
+
+
+def direct_chain(x, weights, dtype):
+    """The same stack with torch direct convolutions in `dtype` (glue identical)."""
+    import torch
+    act, li = x.to(dtype), 0
+    for layer in STACK:
+        if layer == "pool":
+            act = torch.nn.functional.max_pool2d(act, 2)
+            continue
+        act = torch.relu(torch.nn.functional.conv2d(act, weights[li].to(dtype), padding=1))
+        li += 1
+    return torch.nn.functional.max_pool2d(act, 2).double().flatten(1)
+
+
+def proxy(a, x0, weights, finals, rng):
+    import torch
+    import numpy as np
+    n = a.proxy
+    feat = 512 * 7 * 7
+    wfc = torch.from_numpy(rng.normal(0.0, np.sqrt(2.0 / feat), (1000, feat))).cuda()   # He-normal, fan-in feat
+    ref = direct_chain(x0[:n], weights, torch.float64) @ wfc.T
+    top1_ref = ref.argmax(1)
+    res = {"images": n, "classifier": "random He-normal FC 25088 -> 1000 (fp64) after the final max-pool",
+           "reference": "fp64 direct convolutions, same bf16 inputs and weights", "rows": {}}
+    cands = dict(finals)
+    cands["direct_bf16_cudnn"] = direct_chain(x0[:n], weights, torch.bfloat16)
+    for name, f in cands.items():
+        lg = f @ wfc.T
+        top5 = lg.topk(5, dim=1).indices
+        res["rows"][name] = {
+            "top1_agree": float((lg.argmax(1) == top1_ref).double().mean()),
+            "ref_top1_in_top5": float((top5 == top1_ref[:, None]).any(1).double().mean()),
+            "logit_rel_l2": float((lg - ref).norm() / ref.norm()),
+        }
+    return res
 
 
 if __name__ == "__main__":

@@ -34,9 +34,10 @@ def test_library_loads_and_exports_every_symbol():
 
 CONFIGS = [("0,1,-1,inf", 2), ("0,-1,1,-1/2,1/2,inf", 4), ("0,1,-1,2,-2,inf", 4), ("0,a^2+1,inf", 2),
            ("0,-1,a^2+1,inf", 3), ("0,-1,1,a^2+1,inf", 4), ("a^2+1,a^2-2", 2), ("a^3-2,inf", 2), ("a^4+1", 2),
-           ("0,a^2+a+1,inf", 2), ("0,-1,1,a^2-a+1,inf", 4), ("0,-1,1,a^2+1,a^2-2,inf", 6)]
+           ("0,a^2+a+1,inf", 2), ("0,-1,1,a^2-a+1,inf", 4), ("0,-1,1,a^2+1,a^2-2,inf", 6),
+           ("0,1,a^3+a+1,inf", 4), ("0,a^4+1,inf", 4), ("a^3+2,a^2+1,inf", 4)]
 CANON = ["lin2", "lin3", "lin4", "lin5", "lin6", "lin7", "lin8", "sup1_2", "sup1_3", "sup1_4", "sup1_5", "sup1_6",
-         "sup1_7", "sup1_8", "sup2_2", "sup2_4", "sup2_6", "sup2_8"]
+         "sup1_7", "sup1_8", "sup2_2", "sup2_4", "sup2_6", "sup2_8", "lin10", "sup1_10", "sup1_12", "sup2_12"]
 
 
 def _cases():
@@ -108,7 +109,7 @@ def test_parse_moduli():
     ("1,1,-1,inf", 2, 2, "coprime"),
     ("0,-1,inf", 2, 2, "degree budget"),
     ("0,inf,-1,1", 2, 2, "last"),
-    ("0,-1,1,inf", 9, 4, "2 <= m <= 8"),
+    ("0,-1,1,inf", 13, 4, "2 <= m <= 12"),
     ("0,-1,1,-1/2,1/2,2,-2,-1/4,4,1/4,-4,a^2+1,inf", 8, 2, "budget"),
 ])
 def test_config_errors(spec, m, status, needle):

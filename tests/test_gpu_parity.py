@@ -195,8 +195,15 @@ def test_output_transform(dtype, name, lowering):
 # ------------------------------------------------------------------ whole layer
 
 
-def _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad, xdist="relu_normal", seed=0):
-    a, ref, m = algo_pair(name, lowering)
+def algo_pair_spec(spec, m, lowering="subsolver"):
+    mods = T.parse_moduli(spec)
+    a = W.WinoAlgo(spec, m, lowering=lowering)
+    ref = T.make_transforms(mods, m) if lowering == "subsolver" else T.residue_blocks(mods, m)
+    return a, ref, m
+
+
+def _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad, xdist="relu_normal", seed=0, m=None):
+    a, ref, m = algo_pair(name, lowering) if m is None else algo_pair_spec(name, m, lowering)
     x, w = datagen.layer(N, C, K, H, Wd, dtype, seed=seed, xdist=xdist)
     y = W.wino_conv2d(dev(x, dtype), dev(w, dtype), a, pad=pad)
     assert W.wino_last_launch_count() in (3, 4)   # K2, K1, fused K3+K4 | K3, K4
@@ -232,6 +239,9 @@ LAYER_CASES = [
     ("lin4", "subsolver", 1, 3, 64, 224, 224, 1),       # VGG conv1_1: C = 3, 224 wide (3D TMA boxes, column blocks)
     ("lin4", "subsolver", 2, 128, 128, 14, 14, 1),      # VGG block 5 spatial size (flat boxes, 4-row alignment)
     ("sup1_6", "subsolver", 1, 64, 72, 56, 56, 1),      # VGG block 3 spatial size, m = 6
+    ("sup1_10", "subsolver", 1, 64, 64, 25, 27, 1),     # Table 3 W(10x10), mu = 13
+    ("sup1_12", "subsolver", 1, 64, 64, 27, 29, 1),     # Table 3 W(12x12), mu = 15 (reading A21 points)
+    ("sup2_12", "subsolver", 1, 64, 64, 26, 26, 1),     # two quadratics at 12x12, mu = 16
 ]
 
 
@@ -245,6 +255,24 @@ def test_layer(case, dtype):
     elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
     assert sg["nonfinite"] == so["nonfinite"]
+
+
+HIGHER_DEGREE = [("0,1,a^3+a+1,inf", 4), ("0,a^3-2,inf", 3), ("a^3+a+1,inf", 2), ("0,a^4+1,inf", 4),
+                 ("a^4+1,inf", 3), ("a^3+2,a^2+1,inf", 4)]
+
+
+@pytest.mark.parametrize("spec,m", HIGHER_DEGREE)
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_layer_higher_degree_moduli(spec, m, dtype):
+    """Cubic and quartic moduli (Toom-Cook sub-problems on 2d - 1
+    points, domain m + 2 + sum(d - 1) up to m + 5): the layer through the C ABI
+    against the fp64 direct convolution (element-wise error bound) and the
+    oracle's pipeline model."""
+    sg, so, _ = _layer_check(spec, "subsolver", dtype, 2, 72, 40, 19, 23, 1, m=m)
+    if dtype == "fp32":
+        assert sg["rel_l1"] <= 1e-4, sg
+    else:
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])

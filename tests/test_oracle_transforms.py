@@ -405,3 +405,48 @@ def test_scaled_transforms_stay_exact(name):
     if name == "lin8":
         assert max(abs(a) for r in ts.A for a in r) == 16384
         assert max(abs(a) for r in tss.A for a in r) == 4
+
+
+# Moduli of degree 3 and 4 ("1 polynomial of the first degree and 1 of
+# the third degree", "1 polynomial of the fourth degree"; each degree-d modulus
+# is solved by a Toom-Cook sub-problem on 2d - 1 points).
+HIGHER_DEGREE = [("0,1,a^3+a+1,inf", 4), ("0,a^3-2,inf", 3), ("0,a^4+1,inf", 4), ("a^4+1,inf", 3),
+                 ("a^3+2,a^2+1,inf", 4), ("a^3+a+1,inf", 2)]
+
+
+@pytest.mark.parametrize("spec,m", HIGHER_DEGREE)
+def test_exact_higher_degree_moduli(spec, m):
+    """Generated transforms with cubic / quartic moduli compute the exact 1D and
+    2D correlation (rational arithmetic vs brute force), in both lowerings, and
+    the domain grows by 2d - 1 - d = d - 1 per degree-d modulus."""
+    rng = random.Random(hash(spec) & 0xFFFF)
+    mods = T.parse_moduli(spec)
+    ts = T.make_transforms(mods, m)
+    extra = sum(mm.degree - 1 for mm in mods if mm.degree and mm.degree > 1)
+    assert ts.mu == m + 2 + extra
+    rb = T.residue_blocks(mods, m)
+    for _ in range(10):
+        h, x = _rq(rng, 3), _rq(rng, m + 2)
+        ref = CV.direct_corr_1d(h, x)
+        assert CV.winograd_1d_exact(ts, h, x) == ref
+        assert CV.residue_1d_exact(rb, h, x) == ref
+    g = [_rq(rng, 3) for _ in range(3)]
+    d = [_rq(rng, m + 2) for _ in range(m + 2)]
+    assert CV.winograd_2d_exact(ts, g, d) == CV.direct_corr_2d(g, d)
+
+
+@pytest.mark.parametrize("name", ["sup1_8", "sup1_10", "sup1_12", "sup2_12", "lin10"])
+def test_exact_2d_tile_large_tiles(name):
+    """Table 3's W(8x8) .. W(12x12) with one a^2+1, two
+    quadratics at 12x12 and TC(10x10): exact 2D tile correlation in
+    rational arithmetic; mu and the per-output ratio as Section 3.2 counts them."""
+    rng = random.Random(len(name) * 7)
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    extra = 0 if name.startswith("lin") else int(name[3])   # sup1 / sup2: one / two quadratics
+    assert ts.mu == m + 2 + extra
+    if name.startswith("sup1"):
+        assert abs(T.ratio(mods, m) - {8: 1.890625, 10: 1.69, 12: 225 / 144}[m]) < 1e-12   # Table 3 ratios
+    g = [_rq(rng, 3) for _ in range(3)]
+    d = [_rq(rng, m + 2) for _ in range(m + 2)]
+    assert CV.winograd_2d_exact(ts, g, d) == CV.direct_corr_2d(g, d)
