@@ -34,13 +34,15 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--sample", type=int, default=2)
     ap.add_argument("--proxy", type=int, default=32, help="images for the classifier-argmax proxy (0: off)")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
     a = ap.parse_args()
     import numpy as np
     import torch
     import datagen
     import paper_1905_05233_b200 as Wn
     from paper_1905_05233_b200.algos import canonical_spec
-    dt, tdt = "bf16", torch.bfloat16
+    dt = a.dtype
+    tdt = {"bf16": torch.bfloat16, "fp16": torch.float16}[dt]
     rng = np.random.default_rng(0)
     x0 = torch.from_numpy(rng.random((a.n, 3, 224, 224))).to(tdt).cuda()
     weights = []
@@ -49,7 +51,7 @@ def main():
             cin, cout = layer
             w = rng.normal(0.0, datagen.he_sigma(cin), (cout, cin, 3, 3))
             weights.append(torch.from_numpy(w).to(tdt).cuda())
-    out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, bf16, "
+    out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, {dt}, "
                        f"error on {a.sample} images vs fp64 direct", "algos": {}}
     st = torch.cuda.current_stream()
     finals = {}
@@ -119,7 +121,7 @@ def proxy(a, x0, weights, finals, rng):
     res = {"images": n, "classifier": "random He-normal FC 25088 -> 1000 (fp64) after the final max-pool",
            "reference": "fp64 direct convolutions, same bf16 inputs and weights", "rows": {}}
     cands = dict(finals)
-    cands["direct_bf16_cudnn"] = direct_chain(x0[:n], weights, torch.bfloat16)
+    cands[f"direct_{a.dtype}_cudnn"] = direct_chain(x0[:n], weights, x0.dtype)
     for name, f in cands.items():
         lg = f @ wfc.T
         top5 = lg.topk(5, dim=1).indices
