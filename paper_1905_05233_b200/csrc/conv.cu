@@ -13,11 +13,12 @@ wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* a
 wino_status run_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
                                 wino_dtype dt, wino_layout layout, void* V, cudaStream_t st);
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
-                            float* M, cudaStream_t st);
+                            float* M, cudaStream_t st, int mb0 = 0, int nT = -1);
 wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
                                   float* M, void* y, int* done, cudaStream_t st);
 wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
-                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st);
+                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st, int t0 = 0,
+                                 int nT = -1, int Tpm = 0, int disc = 0);
 }  // namespace wino
 
 using namespace wino;
@@ -56,6 +57,20 @@ wino_status wino_conv2d_workspace(const wino_algo* al, int N, int C, int H, int 
   return WINO_OK;
 }
 
+// Tile blocks per K3 -> K4 slice (0: one pass over the whole layer).  Opt-in
+// (WINO_CHUNK_TB=<blocks>, or "auto": slices of M of about 40 MB, well inside the
+// 126 MB L2); NCHW output only.
+static int chunk_blocks(const Geo& g, wino_layout layout) {
+  static const char* e = getenv("WINO_CHUNK_TB");
+  if (!e || layout != WINO_NCHW) return 0;
+  if (std::string(e) == "auto") {
+    const size_t blk = (size_t)g.Q * g.K * 128 * 4;   // M bytes per tile block
+    const int cb = (int)((40u << 20) / (blk ? blk : 1));
+    return cb < 1 ? 1 : cb;
+  }
+  return atoi(e);
+}
+
 wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W, int K, int pad,
                         const wino_algo* al, wino_dtype dt, wino_layout layout, void* out, void* ws,
                         size_t ws_bytes, void* stream) {
@@ -91,6 +106,19 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   if (layout == WINO_NCHW && !fused_disabled()) {
     s = run_domain_gemm_fused(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
     if (s != WINO_E_UNSUPPORTED) return s;   // OK or a real failure
+  }
+  const int cb = chunk_blocks(g, layout);
+  if (cb > 0 && cb < g.TB) {
+    // K3 -> K4 per slice of cb tile blocks through one L2-sized M slice that K4
+    // discards after reading: M never travels to HBM (see chunk_blocks)
+    for (int mb0 = 0; mb0 < g.TB; mb0 += cb) {
+      const int nT = (g.T - mb0 * 128) < cb * 128 ? g.T - mb0 * 128 : cb * 128;
+      if ((s = run_domain_gemm(V, U, g, al, dt, M, st, mb0, nT)) != WINO_OK) return s;
+      if ((s = run_output_transform(M, N, K, H, W, pad, al, dt, layout, out, st, mb0 * 128, nT, (nT + 31) / 32 * 32,
+                                    1)) != WINO_OK)
+        return s;
+    }
+    return WINO_OK;
   }
   if ((s = run_domain_gemm(V, U, g, al, dt, M, st)) != WINO_OK) return s;
   if ((s = run_output_transform(M, N, K, H, W, pad, al, dt, layout, out, st)) != WINO_OK) return s;

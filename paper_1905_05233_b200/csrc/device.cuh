@@ -246,6 +246,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Drop a 128-byte L2 line without writing it back (its contents become undefined):
+// for consumed intermediates that must not cost HBM write bandwidth.
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 }  // namespace wino
 
 // Launch bookkeeping (misc.cu).

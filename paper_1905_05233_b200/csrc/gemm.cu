@@ -56,7 +56,7 @@ template <bool kTF32, int BN, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     domain_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                        const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB, int nNB, int Q, int S,
-                       uint32_t idesc, const __grid_constant__ GemmSched gs) {
+                       uint32_t idesc, const __grid_constant__ GemmSched gs, int mb0, int TBv) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned for the 128-byte swizzle atoms; offsetting the shared array keeps
@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-            tma_load_3d(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi);   // blocked V: one 16 KB block
+            tma_load_3d(base, &tmV, &full[stage], 0, 0, ((mb0 + mb) * KB + kb) * Q + qi);   // blocked V: one 16 KB block
             if constexpr (kTF32)
-              tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], 0, 0, ((nMB + mb) * KB + kb) * Q + qi);
+              tma_load_3d(base + Cfg::A_BYTES, &tmV, &full[stage], 0, 0, ((TBv + mb0 + mb) * KB + kb) * Q + qi);
             uint8_t* bb = base + Cfg::NPL * Cfg::A_BYTES;
             tma_load_3d(bb, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
             if constexpr (kTF32) tma_load_3d(bb + Cfg::B_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl + S);
@@ -227,9 +227,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void discard_l2(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
 // Output transform of one (tile t, channel k) from the TMA-staged M piece
@@ -497,7 +494,7 @@ static int num_sms() {
 
 template <bool kTF32, int BN, int STAGES>
 static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
-                               const GemmSched& gs, uint32_t fmt, cudaStream_t st) {
+                               const GemmSched& gs, uint32_t fmt, int mb0, int nT, cudaStream_t st) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
   auto kern = domain_gemm_kernel<kTF32, BN, STAGES>;
   static bool attr = false;
@@ -505,11 +502,11 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
     WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr = true;
   }
-  const int nMB = (g.T + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
+  const int nMB = (nT + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
   const int items = g.Q * nMB * nNB;
   const int grid = items < num_sms() ? items : num_sms();
-  kern<<<grid, 256, Cfg::SMEM, st>>>(tv, tu, tm, g.T, g.K, g.Cp, nMB, nNB, g.Q, g.S,
-                                     make_idesc(fmt, kBM, BN), gs);
+  kern<<<grid, 256, Cfg::SMEM, st>>>(tv, tu, tm, nT, g.K, g.Cp, nMB, nNB, g.Q, g.S,
+                                     make_idesc(fmt, kBM, BN), gs, mb0, g.TB);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
 }
@@ -606,8 +603,12 @@ wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, co
                         : fused_m<WINO_BF16>(al->m, doff, tv, tu, tm, g, al, fmt, M, y, done, st);
 }
 
+// M_xi for the tiles [mb0 * 128, mb0 * 128 + nT) of V (all of them by default) into
+// M [Q][K][Tpm] with Tpm = nT rounded up to 32 (chunked layers: an L2-sized slice)
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
-                            float* M, cudaStream_t st) {
+                            float* M, cudaStream_t st, int mb0, int nT) {
+  if (nT < 0) nT = g.T;
+  const int Tpm = (nT + 31) / 32 * 32;
   const bool tf32 = dt == WINO_F32;
   CUtensorMapDataType cdt = dt == WINO_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                             : dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -617,19 +618,19 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
   CUtensorMap tv, tu, tm;
   if (!make_map3(&tv, cdt, g.es, V, BK, kBM, (uint64_t)g.planes * g.Q * g.TB * (g.Cp / BK), BK, kBM) ||
       !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
-      !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, g.T, g.K, g.Q, kBM, 32, false, g.Tp)) {
+      !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, nT, g.K, g.Q, kBM, 32, false, Tpm)) {
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
     return WINO_E_CUDA;
   }
   // UMMA operand formats: kind::f16 F16 = 0, BF16 = 1; kind::tf32 TF32 = 2.
   const uint32_t fmt = dt == WINO_F16 ? 0u : dt == WINO_BF16 ? 1u : 2u;
   if (tf32) {
-    if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, st);
-    return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, st);
+    if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+    return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
   }
-  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, st);   // 3 stages + 4 epilogue buffers: 8 % slower
-  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, st);
-  return launch_gemm<false, 64, 8>(tv, tu, tm, g, al->gs, fmt, st);
+  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);   // 3 stages + 4 epilogue buffers: 8 % slower
+  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+  return launch_gemm<false, 64, 8>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
 }
 
 }  // namespace wino

@@ -102,13 +102,15 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
 }
 
 wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
-                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st) {
+                                 wino_dtype dt, wino_layout layout, void* y, cudaStream_t st, int t0, int nT,
+                                 int Tpm, int disc) {
   if ((layout != WINO_NCHW && layout != WINO_NHWC) || !md_ok(al)) {
     set_last_error("output transform: unsupported layout / (m, domain)");
     return WINO_E_UNSUPPORTED;
   }
   Geo g = make_geo(al, N, 1, H, W, K, pad, dt);
-  OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, g.Tp, (int)layout, &al->xp, y, st};
+  OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, nT < 0 ? g.Tp : Tpm, (int)layout, &al->xp, y, st};
+  a.t0 = t0, a.nT = nT, a.disc = disc;
   out_fn_(dt, al->m, al->D - al->m - 2)(a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;

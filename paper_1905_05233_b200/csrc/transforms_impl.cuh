@@ -875,12 +875,16 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
 // One thread per (t, k), t fastest (coalesced reads of M[q][k][t]).  Row-streamed
 // separable transform: Z_i = M_{i,.} A (m values), Y += A_{i,.}^T (x) Z_i.
 template <int DT, int M, int D>
+// Tiles [t0, T) with M rows indexed from t0 (a chunk's M slice when t0 > 0);
+// disc != 0 drops the consumed M lines from L2 afterwards (they are never
+// written back: chunked layers keep M in L2 only).
 __global__ void __launch_bounds__(128) output_transform_nchw(const float* __restrict__ Mw, int K, int Ho, int Wo,
                                                              int th, int tw, int T, int Tp,
                                                              const __grid_constant__ XformParams xp,
-                                                             typename DType<DT>::T* __restrict__ y) {
+                                                             typename DType<DT>::T* __restrict__ y, int t0, int disc) {
   using Tr = DType<DT>;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tl = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = t0 + tl;
   const int k = blockIdx.y;
   if (t >= T) return;
   float Y[M][M];
@@ -889,7 +893,7 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
 #pragma unroll
     for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
   const size_t qs = (size_t)K * Tp;
-  const float* src = Mw + (size_t)k * Tp + t;
+  const float* src = Mw + (size_t)k * Tp + tl;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
     float Mi[D];
@@ -915,6 +919,13 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
   for (int p = 0; p < M; ++p) {
     if (ti * M + p >= Ho) break;
     store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
+  }
+  if (disc) {
+    // every live lane has consumed its M values (they fed Y): lane 0 drops the
+    // warp's 32-tile line of each point
+    __syncwarp(__activemask());
+    if ((threadIdx.x & 31) == 0)
+      for (int q = 0; q < D * D; ++q) discard_l2(src + (size_t)q * qs);
   }
 }
 
@@ -1100,6 +1111,7 @@ struct OutArgs {
   const XformParams* xp;
   void* y;
   cudaStream_t st;
+  int t0 = 0, nT = -1, disc = 0;   // chunked K4 (NCHW thread-per-tile kernel only): tiles [t0, t0 + nT)
 };
 using InFn = void (*)(const InArgs&);
 using OutFn = void (*)(const OutArgs&);
@@ -1271,7 +1283,7 @@ static void launch_in(const InArgs& a) {
 template <int DT, int M, int D>
 static void launch_out(const OutArgs& a) {
   using Tr = DType<DT>;
-  if (a.layout == WINO_NHWC) {
+  if (a.layout == WINO_NHWC && a.nT < 0) {
     const size_t smem = (size_t)32 * K4N<M>::TS * sizeof(typename Tr::T);
     constexpr int KB = K4N<M>::KB;
     auto kern = output_transform_nhwc<DT, M, D>;
@@ -1282,7 +1294,7 @@ static void launch_out(const OutArgs& a) {
   }
   if constexpr (D >= 7) {
     constexpr int Q = D * D;
-    int NB = (int)((96 * 1024) / ((size_t)Q * 128 * 4));
+    int NB = a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * 4)) : 0;   // chunks: thread-per-tile kernel
     NB = NB > 4 ? 4 : NB;
     CUtensorMap tml;
     const uint64_t dims[3] = {(uint64_t)a.Tp, (uint64_t)a.K, (uint64_t)Q};
@@ -1298,9 +1310,10 @@ static void launch_out(const OutArgs& a) {
       return;
     }
   }
-  dim3 grid((a.T + 127) / 128, a.K);
-  output_transform_nchw<DT, M, D><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp,
-                                                          (typename Tr::T*)a.y);
+  const int nT = a.nT < 0 ? a.T - a.t0 : a.nT;
+  dim3 grid((nT + 127) / 128, a.K);
+  output_transform_nchw<DT, M, D><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT, a.Tp,
+                                                          *a.xp, (typename Tr::T*)a.y, a.t0, a.disc);
 }
 
 // m in [2, 8], domain D in [m + 2, m + 4] (at most two quadratic moduli).

@@ -452,6 +452,46 @@ def test_vgg16_stack_per_layer(name):
     assert li == 13
 
 
+def test_chunked_layer_matches_one_pass():
+    """WINO_CHUNK_TB=<blocks>: K3 -> K4 per slice of tile blocks through one
+    L2-resident M slice that K4 discards after reading.  Same fp32 arithmetic per
+    output, so y is bit-identical to the one-pass layer (ragged last slice, D < 7
+    and D >= 7).  Subprocesses: the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    code = r"""
+import sys, torch, numpy as np
+sys.path.insert(0, '.')
+import datagen, paper_1905_05233_b200 as W
+from paper_1905_05233_b200.algos import canonical_spec
+out = []
+for name, dt, N in (('lin4', 'bf16', 7), ('sup1_6', 'fp16', 5), ('lin3', 'fp32', 3)):
+    spec, m = canonical_spec(name)
+    a = W.WinoAlgo(spec, m)
+    x, w = datagen.layer(N, 80, 136, 29, 31, dt, seed=4)
+    td = {'bf16': torch.bfloat16, 'fp16': torch.float16, 'fp32': torch.float32}[dt]
+    y = W.wino_conv2d(torch.from_numpy(x).to(td).cuda(), torch.from_numpy(w).to(td).cuda(), a)
+    torch.cuda.synchronize()
+    out.append(y.float().cpu().numpy().ravel())
+np.save(sys.argv[1], np.concatenate(out))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for chunk in ("", "2", "1"):
+        f = tempfile.NamedTemporaryFile(suffix=".npy", delete=False).name
+        env = dict(os.environ)
+        env.pop("WINO_CHUNK_TB", None)
+        if chunk:
+            env["WINO_CHUNK_TB"] = chunk
+        r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1]) and np.array_equal(res[0], res[2])
+
+
 def test_fused_gemm_output_transform_matches_staged():
     """The opt-in fused K3+K4 kernel (WINO_FUSED=1, output transform from L2) gives
     bit-identical y to the staged K3 -> K4 pair (same fp32 arithmetic per
