@@ -874,14 +874,14 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
 // ------------------------------------------------------------------ K4 output transform (NCHW)
 // One thread per (t, k), t fastest (coalesced reads of M[q][k][t]).  Row-streamed
 // separable transform: Z_i = M_{i,.} A (m values), Y += A_{i,.}^T (x) Z_i.
-template <int DT, int M, int D>
 // Tiles [t0, T) with M rows indexed from t0 (a chunk's M slice when t0 > 0);
-// disc != 0 drops the consumed M lines from L2 afterwards (they are never
-// written back: chunked layers keep M in L2 only).
+// DISC drops the consumed M lines from L2 afterwards (they are never written
+// back: chunked layers keep M in L2 only).
+template <int DT, int M, int D, bool DISC>
 __global__ void __launch_bounds__(128) output_transform_nchw(const float* __restrict__ Mw, int K, int Ho, int Wo,
                                                              int th, int tw, int T, int Tp,
                                                              const __grid_constant__ XformParams xp,
-                                                             typename DType<DT>::T* __restrict__ y, int t0, int disc) {
+                                                             typename DType<DT>::T* __restrict__ y, int t0) {
   using Tr = DType<DT>;
   const int tl = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = t0 + tl;
@@ -920,7 +920,7 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
     if (ti * M + p >= Ho) break;
     store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
   }
-  if (disc) {
+  if constexpr (DISC) {
     // every live lane has consumed its M values (they fed Y): lane 0 drops the
     // warp's 32-tile line of each point
     __syncwarp(__activemask());
@@ -1312,8 +1312,12 @@ static void launch_out(const OutArgs& a) {
   }
   const int nT = a.nT < 0 ? a.T - a.t0 : a.nT;
   dim3 grid((nT + 127) / 128, a.K);
-  output_transform_nchw<DT, M, D><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT, a.Tp,
-                                                          *a.xp, (typename Tr::T*)a.y, a.t0, a.disc);
+  if (a.disc)
+    output_transform_nchw<DT, M, D, true><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT, a.Tp,
+                                                                  *a.xp, (typename Tr::T*)a.y, a.t0);
+  else
+    output_transform_nchw<DT, M, D, false><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT,
+                                                                   a.Tp, *a.xp, (typename Tr::T*)a.y, a.t0);
 }
 
 // m in [2, 8], domain D in [m + 2, m + 4] (at most two quadratic moduli).
