@@ -135,28 +135,56 @@ wino_status wino_conv2d_host_io(const void* x_host, void* x_dev, const void* w_d
   Geo g = make_geo(al, N, C, H, W, K, pad, dt);
   if (ws_bytes < g.total) return set_last_error("workspace too small"), WINO_E_WORKSPACE;
   // Images are independent (P:498 tiles never cross images), so the batch is
-  // processed in (up to 8) chunks: the H2D copy of chunk j+1 and the D2H copy of chunk
-  // j-1 (two library-owned copy streams, opposite PCIe directions) overlap the
-  // layer on chunk j (the caller's stream).  The caller's stream finally waits
-  // for the last copy, so synchronising it covers everything.
+  // processed in chunks: the H2D copy of chunk j+1 and the D2H copy of chunk j-1
+  // (two library-owned copy streams, opposite PCIe directions) overlap the layer
+  // on chunk j (the caller's stream).  The layer is far faster than PCIe, so
+  // the time is the copies plus the pipeline's fill and drain -- the first
+  // chunk's H2D and the last chunk's D2H.  Chunk sizes therefore ramp up
+  // geometrically from one image to N/8 and back down (1, 1, 2, 2, 4, 4, ...
+  // ..., 4, 2, 1), which makes the fill and drain a few images long.  The
+  // caller's stream finally waits for the last copy, so synchronising it
+  // covers everything.
   const size_t xi = (size_t)C * H * W * g.es, yi = (size_t)K * g.Ho * g.Wo * g.es;   // bytes per image
-  const int nch = N >= 8 ? 8 : N;
+  int plan[63], nch = 0;
+  {
+    static const int kUniform = [] {   // tuning knob: WINO_HOSTIO_CHUNKS=<n> equal chunks instead
+      const char* e = getenv("WINO_HOSTIO_CHUNKS");
+      const int v = e ? atoi(e) : 0;
+      return v < 0 ? 0 : (v > 63 ? 63 : v);
+    }();
+    if (kUniform) {
+      nch = N >= kUniform ? kUniform : N;
+      for (int j = 0; j < nch; ++j) plan[j] = N / nch + (j < N % nch ? 1 : 0);
+    } else {
+      int head[32], tail[32], nh = 0, nt = 0, rem = N, sz = 1;
+      const int cap = N / 8 > 1 ? N / 8 : 1;
+      while (rem > 0 && nh + nt < 61) {
+        head[nh] = sz < rem ? sz : rem, rem -= head[nh++];
+        if (rem <= 0) break;
+        tail[nt] = sz < rem ? sz : rem, rem -= tail[nt++];
+        if (sz < cap) sz = 2 * sz < cap ? 2 * sz : cap;
+      }
+      for (int j = 0; j < nh; ++j) plan[nch++] = head[j];
+      if (rem > 0) plan[nch++] = rem;   // (chunk-count limit reached)
+      for (int j = nt - 1; j >= 0; --j) plan[nch++] = tail[j];
+    }
+  }
   static thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
-  static thread_local cudaEvent_t ev[2][16];
+  static thread_local cudaEvent_t ev[2][64];
   if (!s_in) {
     WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
     WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
     for (int a = 0; a < 2; ++a)
-      for (int j = 0; j < 16; ++j) WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev[a][j], cudaEventDisableTiming));
+      for (int j = 0; j < 64; ++j) WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev[a][j], cudaEventDisableTiming));
   }
   // copies must not start before work already queued on the caller's stream
-  cudaEvent_t start = ev[1][15];
+  cudaEvent_t start = ev[1][63];
   WINO_CUDA_CHECK(cudaEventRecord(start, st));
   WINO_CUDA_CHECK(cudaStreamWaitEvent(s_in, start, 0));
   WINO_CUDA_CHECK(cudaStreamWaitEvent(s_out, start, 0));
   int launches = 0;
   for (int j = 0, n0 = 0; j < nch; ++j) {
-    const int nj = N / nch + (j < N % nch ? 1 : 0);
+    const int nj = plan[j];
     char* xd = static_cast<char*>(x_dev) + (size_t)n0 * xi;
     char* yd = static_cast<char*>(out_dev) + (size_t)n0 * yi;
     WINO_CUDA_CHECK(cudaMemcpyAsync(xd, static_cast<const char*>(x_host) + (size_t)n0 * xi, (size_t)nj * xi,
@@ -172,8 +200,8 @@ wino_status wino_conv2d_host_io(const void* x_host, void* x_dev, const void* w_d
                                     cudaMemcpyDeviceToHost, s_out));
     n0 += nj;
   }
-  WINO_CUDA_CHECK(cudaEventRecord(ev[0][15], s_out));
-  WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev[0][15], 0));
+  WINO_CUDA_CHECK(cudaEventRecord(ev[0][63], s_out));
+  WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev[0][63], 0));
   reset_launch_count();
   count_launch(launches);
   return WINO_OK;
