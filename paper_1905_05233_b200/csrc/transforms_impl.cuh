@@ -123,11 +123,19 @@ __global__ void __launch_bounds__(128) weight_transform_points(const typename DT
 // The transform loops are fully unrolled, so a false nz() removes the term's
 // FFMA2 (the coefficient values stay runtime kernel parameters).  Skipping a
 // zero term can only change the sign of an exact zero result.
+// Row pairs (small tiles only): rows j1 < j2 of B^T with B^T[j2][q] = +-B^T[j1][q]
+// (Toom-Cook points +-p, P:533's good points come in such pairs).  Then
+// E = sum_{q: +} B^T[j1][q] x_q, O = sum_{q: -} B^T[j1][q] x_q give both rows as
+// E + O and E - O, and in the second stage the two output rows accumulate E and
+// O once instead of twice.  PAIRS holds 4 bits per row (partner + 1, 0 = none),
+// NEG bit j1 * n_x + q marks the '-' columns of base row j1.
 struct DenseBT {
   __host__ __device__ static constexpr bool nz(int, int, int) { return true; }
   __host__ __device__ static constexpr int first(int, int) { return 0; }
+  __host__ __device__ static constexpr int partner(int) { return -1; }
+  __host__ __device__ static constexpr bool neg(int, int, int) { return false; }
 };
-template <uint64_t W0, uint64_t W1>
+template <uint64_t W0, uint64_t W1, uint64_t PAIRS = 0, uint64_t NEG = 0>
 struct MaskBT {
   __host__ __device__ static constexpr bool nz(int j, int q, int nx) {
     return j * nx + q < 64 ? ((W0 >> (j * nx + q)) & 1) != 0 : ((W1 >> (j * nx + q - 64)) & 1) != 0;
@@ -137,7 +145,76 @@ struct MaskBT {
     while (a < nx && !nz(i, a, nx)) ++a;
     return a;
   }
+  __host__ __device__ static constexpr int partner(int j) { return (int)((PAIRS >> (4 * j)) & 15) - 1; }
+  __host__ __device__ static constexpr bool neg(int j1, int q, int nx) { return ((NEG >> (j1 * nx + q)) & 1) != 0; }
 };
+
+// Small-tile core shared by every K1 staging path (so they stay bit-identical):
+// V = B^T d B with the first stage per output column j and the second stage per
+// output row i, row pairs folded as above.  load_row(a, d) fills input row a.
+template <int DT, int NX, int D, typename MK, typename LoadRow>
+__device__ __forceinline__ void transform_tile_small(LoadRow load_row, const XformParams& xp,
+                                                     typename DType<DT>::T* out, size_t qstride, size_t plane) {
+  float2 acc[D][D];
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int a = 0; a < NX; ++a) {
+    float2 d[NX];
+    load_row(a, d);
+    float2 rt[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int p = MK::partner(j);
+      if (p >= 0 && p < j) continue;   // the second row of a pair: formed with its base row
+      float2 e = make_float2(0.f, 0.f), o = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < NX; ++q) {
+        const float c = xp.BT[j][q];
+        if (!MK::nz(j, q, NX)) continue;
+        if (p > j && MK::neg(j, q, NX)) o = __ffma2_rn(d[q], make_float2(c, c), o);
+        else e = __ffma2_rn(d[q], make_float2(c, c), e);
+      }
+      if (p > j) {
+        rt[j] = __ffma2_rn(o, make_float2(1.f, 1.f), e);
+        rt[p] = __ffma2_rn(o, make_float2(-1.f, -1.f), e);
+      } else {
+        rt[j] = e;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      const int p = MK::partner(i);
+      if (p >= 0 && p < i) continue;   // accumulated into its base row's E / O slots
+      const float c = xp.BT[i][a];
+      if (!MK::nz(i, a, NX)) continue;
+      // paired rows: acc[i] collects E, acc[p] collects O until the end
+      const int dst = (p > i && MK::neg(i, a, NX)) ? p : i;
+#pragma unroll
+      for (int j = 0; j < D; ++j)
+        acc[dst][j] = (p < 0 && a == MK::first(i, NX)) ? __fmul2_rn(rt[j], make_float2(c, c))
+                                                       : __ffma2_rn(rt[j], make_float2(c, c), acc[dst][j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    const int p = MK::partner(i);
+    if (p > i) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const float2 e = acc[i][j], o = acc[p][j];
+        acc[i][j] = __ffma2_rn(o, make_float2(1.f, 1.f), e);
+        acc[p][j] = __ffma2_rn(o, make_float2(-1.f, -1.f), e);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < D; ++i)
+#pragma unroll
+    for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
+}
 
 // ------------------------------------------------------------------ K1 input transform (NCHW)
 // Channel-pair design for sm_100a.  CTA = (tile-column block of TJB tiles,
@@ -226,50 +303,19 @@ __host__ __device__ constexpr int k1_jc(int NX, int D) { return k1_nchunk(NX, D)
 // The separable transform runs on packed FFMA2 (coefficient broadcast); each
 // V_q store of the warp is one contiguous 128-byte (16-bit) / 2 x 256-byte
 // (fp32 hi/lo) row of the K-major GEMM operand.
-template <int DT, int NX, int D>
+template <int DT, int NX, int D, typename MK = DenseBT>
 __device__ __forceinline__ void transform_tile_pairs(const float2* ring, int s0, int SEG, int col,
                                                      const XformParams& xp, typename DType<DT>::T* out,
                                                      size_t qstride, size_t plane) {
   constexpr int JC = k1_jc(NX, D);
   if constexpr (k1_nchunk(NX, D) == 1) {
-    // small tiles: everything unrolled (coefficients in uniform registers),
-    // in FJ-column chunks separated by a memory clobber so the scheduler
-    // cannot interleave them (D x FJ accumulators live, not D x D)
-    constexpr int FJ = NX * D > 24 ? (D + 1) / 2 : D;
+    auto load_row = [&](int a, float2* d) {
+      const int sa = s0 + a < NX ? s0 + a : s0 + a - NX;
+      const float2* sd = ring + (sa * SEG + col) * 32;
 #pragma unroll
-    for (int j0 = 0; j0 < D; j0 += FJ) {
-      float2 acc[D][FJ];
-#pragma unroll
-      for (int a = 0; a < NX; ++a) {
-        const int sa = s0 + a < NX ? s0 + a : s0 + a - NX;
-        const float2* sd = ring + (sa * SEG + col) * 32;
-        float2 d[NX];
-#pragma unroll
-        for (int q = 0; q < NX; ++q) d[q] = sd[q * 32];
-#pragma unroll
-        for (int jj = 0; jj < FJ; ++jj) {
-          if (j0 + jj < D) {
-            float2 rt = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int q = 0; q < NX; ++q) {
-              const float c = xp.BT[j0 + jj][q];
-              rt = __ffma2_rn(d[q], make_float2(c, c), rt);
-            }
-#pragma unroll
-            for (int i = 0; i < D; ++i) {
-              const float c = xp.BT[i][a];
-              acc[i][jj] = a == 0 ? __fmul2_rn(rt, make_float2(c, c)) : __ffma2_rn(rt, make_float2(c, c), acc[i][jj]);
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int jj = 0; jj < FJ; ++jj)
-          if (j0 + jj < D) store_pair<DT>(out + (size_t)(i * D + j0 + jj) * qstride, acc[i][jj], plane);
-      asm volatile("" ::: "memory");
-    }
+      for (int q = 0; q < NX; ++q) d[q] = sd[q * 32];
+    };
+    transform_tile_small<DT, NX, D, MK>(load_row, xp, out, qstride, plane);
   } else {
     // larger tiles: JC output columns at a time and a rolled loop over input
     // rows, so only D x JC accumulators and one halo row live in registers
@@ -362,39 +408,13 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
   using P = PairT<DT>;
   constexpr int JC = k1_jc(NX, D);
   if constexpr (k1_nchunk(NX, D) == 1) {
-    float2 acc[D][D];
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) acc[i][j] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int a = 0; a < NX; ++a) {
+    auto load_row = [&](int a, float2* d) {
       const int sa = s0 + a < RR ? s0 + a : s0 + a - RR;
       const PT* sd = ring + sa * 32 * SEGP + col;
-      float2 d[NX];
 #pragma unroll
       for (int q = 0; q < NX; ++q) d[q] = P::unpack(sd[q]);
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        float2 rt = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < NX; ++q) {
-          const float c = xp.BT[j][q];
-          if (MK::nz(j, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
-        }
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          const float c = xp.BT[i][a];
-          if (MK::nz(i, a, NX))
-            acc[i][j] = a == MK::first(i, NX) ? __fmul2_rn(rt, make_float2(c, c))
-                                              : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
+    };
+    transform_tile_small<DT, NX, D, MK>(load_row, xp, out, qstride, plane);
   } else {
     // JC output columns per pass; small enough domains unroll every pass
     // (compile-time coefficient indices) with a memory clobber between passes
@@ -649,36 +669,7 @@ __device__ __forceinline__ void transform_tile_box(const PT* box, int BOXW, int 
     }
   };
   if constexpr (k1_nchunk(NX, D) == 1) {
-    float2 acc[D][D];
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) acc[i][j] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int a = 0; a < NX; ++a) {
-      float2 d[NX];
-      load_row(a, d);
-#pragma unroll
-      for (int j = 0; j < D; ++j) {
-        float2 rt = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < NX; ++q) {
-          const float c = xp.BT[j][q];
-          if (MK::nz(j, q, NX)) rt = __ffma2_rn(d[q], make_float2(c, c), rt);
-        }
-#pragma unroll
-        for (int i = 0; i < D; ++i) {
-          const float c = xp.BT[i][a];
-          if (MK::nz(i, a, NX))
-            acc[i][j] = a == MK::first(i, NX) ? __fmul2_rn(rt, make_float2(c, c))
-                                              : __ffma2_rn(rt, make_float2(c, c), acc[i][j]);
-        }
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-      for (int j = 0; j < D; ++j) store_pair<DT>(out + (size_t)(i * D + j) * qstride, acc[i][j], plane);
+    transform_tile_small<DT, NX, D, MK>(load_row, xp, out, qstride, plane);
   } else {
     // JC output columns per pass; small enough domains unroll every pass
     // (compile-time coefficient indices) with a memory clobber between passes
@@ -789,7 +780,7 @@ __global__ void __launch_bounds__(256, 2) input_transform_nhwc(const __grid_cons
 
 // Fallback for NHWC tensors TMA cannot describe (C * es % 16 != 0, e.g. C = 3):
 // thread per (tile, channel pair), direct loads of the halo from global memory.
-template <int DT, int M, int NX, int D>
+template <int DT, int M, int NX, int D, typename MK = DenseBT>
 __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typename DType<DT>::T* __restrict__ x, int C,
                                                                    int H, int W, int pad, int th, int tw, int Cp,
                                                                    int T, const __grid_constant__ XformParams xp,
@@ -801,6 +792,21 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
   if (2 * pi >= Cp) return;
   const int ca = 2 * pi, cb = ca + 1;
   const int tj = t % tw, rest = t / tw, ti = rest % th, n = rest / th;
+  if constexpr (k1_nchunk(NX, D) == 1) {
+    auto load_row = [&](int a, float2* d) {
+      const int r = ti * M - pad + a;
+#pragma unroll
+      for (int q = 0; q < NX; ++q) {
+        const int c = tj * M - pad + q;
+        const bool ok = r >= 0 && r < H && c >= 0 && c < W;
+        const typename Tr::T* px = x + (((size_t)n * H + (ok ? r : 0)) * W + (ok ? c : 0)) * C;
+        d[q] = make_float2(ok && ca < C ? Tr::load(px + ca) : 0.f, ok && cb < C ? Tr::load(px + cb) : 0.f);
+      }
+    };
+    transform_tile_small<DT, NX, D, MK>(load_row, xp, V + v_offset(t, ca, Cp, 128 / (int)sizeof(typename Tr::T), D * D),
+                                        kVPointBytes / sizeof(typename Tr::T), plane);
+    return;
+  }
   float2 rowT[NX][D];
 #pragma unroll
   for (int a = 0; a < NX; ++a) {
@@ -836,7 +842,7 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
 
 // Synchronous variant for rows whose vectors are narrower than 4 bytes (odd W
 // in 16-bit): CTA = (tile-column block, (n, ti), channel block).
-template <int DT, int M, int NX, int D>
+template <int DT, int M, int NX, int D, typename MK = DenseBT>
 __global__ void __launch_bounds__(256, 2) input_transform_pairs(
     const typename DType<DT>::T* __restrict__ x, int C, int H, int W, int pad, int th, int tw, int Cp, int TJB, int VEC,
     const __grid_constant__ XformParams xp, typename DType<DT>::T* __restrict__ V, size_t qstride, size_t plane) {
@@ -866,7 +872,7 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
     const int tj = tj0 + tjl;
     if (tj >= tw) break;
     const size_t t = ((size_t)n * th + ti) * tw + tj;
-    transform_tile_pairs<DT, NX, D>(s2 + lane, 0, SEG, tjl * M, xp, V + v_offset((int)t, ca, Cp, 128 / (int)sizeof(TT), D * D),
+    transform_tile_pairs<DT, NX, D, MK>(s2 + lane, 0, SEG, tjl * M, xp, V + v_offset((int)t, ca, Cp, 128 / (int)sizeof(TT), D * D),
                                     kVPointBytes / sizeof(TT), plane);
   }
 }
@@ -1116,40 +1122,87 @@ struct OutArgs {
 using InFn = void (*)(const InArgs&);
 using OutFn = void (*)(const OutArgs&);
 
-// B^T zero pattern of the runtime algorithm (bit j * n_x + q, as in bt_masks.hpp)
-inline void bt_mask(const XformParams& xp, int nx, int D, uint64_t& w0, uint64_t& w1) {
-  w0 = w1 = 0;
+// B^T structure of the runtime algorithm, computed exactly as scripts/gen_bt_masks.py
+// does for bt_masks.hpp: zero pattern (bit j * n_x + q) and, for fully unrolled
+// small tiles, the +-row pairs (greedy in row order) with their '-' columns.
+struct BTKey {
+  uint64_t w0 = 0, w1 = 0, pairs = 0, neg = 0;
+};
+inline BTKey bt_key(const XformParams& xp, int nx, int D) {
+  BTKey k;
   for (int j = 0; j < D; ++j)
     for (int q = 0; q < nx; ++q)
       if (xp.BT[j][q] != 0.f) {
         const int b = j * nx + q;
-        (b < 64 ? w0 : w1) |= 1ull << (b & 63);
+        (b < 64 ? k.w0 : k.w1) |= 1ull << (b & 63);
       }
+  if (nx * D > 36) return k;
+  int partner[16];
+  for (int j = 0; j < D; ++j) partner[j] = -1;
+  for (int j1 = 0; j1 < D; ++j1) {
+    if (partner[j1] >= 0) continue;
+    for (int j2 = j1 + 1; j2 < D; ++j2) {
+      if (partner[j2] >= 0) continue;
+      bool ok = true, flip = false;
+      for (int q = 0; q < nx && ok; ++q) {
+        const float u = xp.BT[j1][q], v = xp.BT[j2][q];
+        if (v == u) continue;
+        if (v == -u) flip = true;
+        else ok = false;
+      }
+      if (!ok || !flip) continue;
+      partner[j1] = j2, partner[j2] = j1;
+      for (int q = 0; q < nx; ++q)
+        if (xp.BT[j1][q] != 0.f && xp.BT[j2][q] == -xp.BT[j1][q]) k.neg |= 1ull << (j1 * nx + q);
+      break;
+    }
+  }
+  for (int j = 0; j < D; ++j) k.pairs |= (uint64_t)(partner[j] + 1) << (4 * j);
+  return k;
 }
-// K1 kernel for the algorithm's zero pattern: a compiled zero-skipping instance
-// when the pattern is one of bt_masks.hpp, else the dense one
+// K1 kernels for the algorithm's B^T structure: a compiled instance when it is
+// one of bt_masks.hpp, else the dense one
+#define WINO_PICK(nx_, d_, a_, b_, p_, n_)                                                         \
+  if constexpr (nx_ == NX && d_ == D) {                                                            \
+    if (k.w0 == a_ && k.w1 == b_ && k.pairs == p_ && k.neg == n_) kern = KERN<DT, M, NX, D, MaskBT<a_, b_, p_, n_>>; \
+  }
 template <int DT, int M, int NX, int D>
 static auto pick_k1_tma(const XformParams& xp) {
-  auto kern = input_transform_tma<DT, M, NX, D, DenseBT>;
-  uint64_t w0, w1;
-  bt_mask(xp, NX, D, w0, w1);
-#define WINO_PICK(nx_, d_, a_, b_) \
-  if constexpr (nx_ == NX && d_ == D) { if (w0 == a_ && w1 == b_) kern = input_transform_tma<DT, M, NX, D, MaskBT<a_, b_>>; }
+#define KERN input_transform_tma
+  auto kern = KERN<DT, M, NX, D, DenseBT>;
+  const BTKey k = bt_key(xp, NX, D);
   WINO_BT_MASKS(WINO_PICK)
-#undef WINO_PICK
+#undef KERN
   return kern;
 }
 template <int DT, int M, int NX, int D>
 static auto pick_k1_nhwc(const XformParams& xp) {
-  auto kern = input_transform_nhwc<DT, M, NX, D, DenseBT>;
-  uint64_t w0, w1;
-  bt_mask(xp, NX, D, w0, w1);
-#define WINO_PICK(nx_, d_, a_, b_) \
-  if constexpr (nx_ == NX && d_ == D) { if (w0 == a_ && w1 == b_) kern = input_transform_nhwc<DT, M, NX, D, MaskBT<a_, b_>>; }
+#define KERN input_transform_nhwc
+  auto kern = KERN<DT, M, NX, D, DenseBT>;
+  const BTKey k = bt_key(xp, NX, D);
   WINO_BT_MASKS(WINO_PICK)
-#undef WINO_PICK
+#undef KERN
   return kern;
 }
+template <int DT, int M, int NX, int D>
+static auto pick_k1_nhwc_direct(const XformParams& xp) {
+#define KERN input_transform_nhwc_direct
+  auto kern = KERN<DT, M, NX, D, DenseBT>;
+  const BTKey k = bt_key(xp, NX, D);
+  WINO_BT_MASKS(WINO_PICK)
+#undef KERN
+  return kern;
+}
+template <int DT, int M, int NX, int D>
+static auto pick_k1_pairs(const XformParams& xp) {
+#define KERN input_transform_pairs
+  auto kern = KERN<DT, M, NX, D, DenseBT>;
+  const BTKey k = bt_key(xp, NX, D);
+  WINO_BT_MASKS(WINO_PICK)
+#undef KERN
+  return kern;
+}
+#undef WINO_PICK
 
 template <int DT, int M, int D>
 static void launch_in_nhwc(const InArgs& a) {
@@ -1187,7 +1240,7 @@ static void launch_in_nhwc(const InArgs& a) {
   }
   const int T = a.N * a.th * a.tw;
   dim3 grid((a.Cp / 2 + 127) / 128, T);
-  input_transform_nhwc_direct<DT, M, NX, D><<<grid, 128, 0, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th,
+  pick_k1_nhwc_direct<DT, M, NX, D>(*a.xp)<<<grid, 128, 0, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th,
                                                                       a.tw, a.Cp, T, *a.xp, (TT*)a.V, a.qstride,
                                                                       a.plane);
 }
@@ -1274,7 +1327,7 @@ static void launch_in(const InArgs& a) {
       vec = (int)(b / es);
       break;
     }
-  auto kern = input_transform_pairs<DT, M, NX, D>;
+  auto kern = pick_k1_pairs<DT, M, NX, D>(*a.xp);
   if (ring > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ring);
   dim3 grid((a.tw + tjb - 1) / tjb, a.N * a.th, a.Cp / 64);
   kern<<<grid, 32 * tjb, ring, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th, a.tw, a.Cp, tjb, vec, *a.xp,
