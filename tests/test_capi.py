@@ -172,3 +172,14 @@ def test_scale_errors():
     with pytest.raises(W.WinoError) as e:
         r.scale("pow2")
     assert e.value.status == 4
+
+
+def test_bt_masks_header_in_sync():
+    """csrc/bt_masks.hpp (B^T zero patterns and +-row pairs baked into K1) equals what
+    scripts/gen_bt_masks.py derives from the generator now; a stale header would only
+    cost speed (the runtime key would not match), this keeps it honest."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "gen_bt_masks.py"), "--check"], cwd=root)
+    assert r.returncode == 0
