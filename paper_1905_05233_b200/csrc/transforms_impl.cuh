@@ -1230,13 +1230,17 @@ static void launch_in_nhwc(const InArgs& a) {
     const uint32_t box[4] = {64, (uint32_t)gk.BOXW, (uint32_t)NX, 1};
     ok = make_map(&tm, cdt, 4, a.x, dims, str, box, false);
   }
-  if (ok) {
-    auto kern = pick_k1_nhwc<DT, M, NX, D>(*a.xp);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
-    const int cw = gk.TJB < 7 ? gk.TJB : 7;   // compute warps (+1 TMA producer warp)
-    kern<<<grid, 32 * (cw + 1), smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
-    return;
+  // (tiles beyond 8x8 take the direct-load kernel: their boxes rarely fit, and
+  // not instantiating the TMA kernels for them halves the build time)
+  if constexpr (M <= 8) {
+    if (ok) {
+      auto kern = pick_k1_nhwc<DT, M, NX, D>(*a.xp);
+      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
+      const int cw = gk.TJB < 7 ? gk.TJB : 7;   // compute warps (+1 TMA producer warp)
+      kern<<<grid, 32 * (cw + 1), smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
+      return;
+    }
   }
   const int T = a.N * a.th * a.tw;
   dim3 grid((a.Cp / 2 + 127) / 128, T);
@@ -1306,8 +1310,8 @@ static void launch_in(const InArgs& a) {
       smem = 256 + (size_t)gk.NSLOT * gk.slot_bytes + (size_t)gk.RR * 32 * gk.SEGP * sizeof(PT);
       if (smem <= 110 * 1024) break;
     }
-    ok = smem <= 200 * 1024;
-    if (ok) {
+    ok = smem <= 200 * 1024 && M <= 8;   // tiles beyond 8x8: synchronous staging (see launch_in_nhwc)
+    if constexpr (M <= 8) if (ok) {
       auto kern = pick_k1_tma<DT, M, NX, D>(*a.xp);
       if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       constexpr int MAXCW = k1_maxcw(NX, D);
