@@ -5,10 +5,13 @@ Winograd-domain GEMM, K4 output transform) over one batch of synthetic input.
 
 Default workload (BASELINE.json configs[4], the largest single-GPU config the
 metric is quoted on): N=256, C=K=512, 28x28, pad 1, post-ReLU inputs, He
-weights; F(4x4, 3x3) Toom-Cook {0,-1,1,-1/2,1/2,inf} in bf16.  Under torchrun
-every rank runs its own N=256 images (weak scaling: the layer partitions over
-the batch with no exchange step); the only collective is the
-NCCL all-reduce of the error statistics, outside the timed region.
+weights; F(4x4, 3x3) Toom-Cook {0,-1,1,-1/2,1/2,inf} in bf16.  With --gpus N
+(N > 1) the script re-launches itself under torchrun as N ranks, one per GPU
+(NCCL); the global batch of 256 images is drawn once and split over the ranks
+(strong scaling: the layer partitions over the batch with no exchange step,
+DESIGN.md 8; --scaling weak gives every rank the whole batch).  The only
+collective is the NCCL all-reduce of the error statistics, outside the timed
+region.  Each rank's step is captured as one CUDA graph (--graph off: eager).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--algo lin4] [--dtype bf16]
     python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
@@ -49,6 +52,10 @@ def parse():
                     help="activation layout of x and y (BASELINE's x[N,C,H,W] is nchw)")
     ap.add_argument("--sweep", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--no-extras", action="store_true", help="timed loop only (for ncu launch lists)")
+    ap.add_argument("--no-dtypes", action="store_true", help="skip the per-dtype roofline legs")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: the workload's global batch is split over the ranks; weak: every rank runs it")
+    ap.add_argument("--graph", default="on", choices=["on", "off"], help="time the step as one CUDA graph")
     return ap.parse_args()
 
 
@@ -153,7 +160,7 @@ def run_reference(a, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": a.gpus,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
+        "scaling": a.scaling, "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
         "config": {"workload": c["desc"], "algo": f"{a.algo} {{{T.moduli_spec(mods)}}}", "sample": sample},
         "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -191,17 +198,61 @@ def cpu_baseline(algo_name, dtype, c, budget_s=20.0):
             "sample": f"{n} of {c['N']} images, {dt:.1f} s (pipeline-mode emulation of {algo_name} {dtype})"}
 
 
+# --------------------------------------------------------------------------- launcher
+
+
+def launcher_cmd(argv, gpus, port, script=None):
+    """torchrun command that re-runs this script (or `script`) as `gpus` ranks
+    (one process per GPU, NCCL; rendezvous on 127.0.0.1).  Used when
+    `--gpus N > 1` is given without a torchrun environment."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", script or os.path.abspath(__file__)] + list(argv)
+
+
+def self_launch(a):
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    return subprocess.call(launcher_cmd(sys.argv[1:], a.gpus, port))
+
+
+def rank_batch(n_global, world, rank, scaling):
+    """Images [lo, hi) of the globally generated batch this rank runs.  Strong
+    scaling (default): the global batch of the workload is split evenly over the
+    ranks (paper_1905_05233_b200.distributed.batch_slice).  Weak scaling: every
+    rank runs the whole workload batch (the same images, so the statistics stay
+    comparable across rank counts)."""
+    from paper_1905_05233_b200 import distributed as D
+    if scaling == "weak":
+        return 0, n_global
+    return D.batch_slice(n_global, world, rank)
+
+
 # --------------------------------------------------------------------------- our arm
+
+
+def tc_peak_tflops(dtype, peaks):
+    """Tensor peak for the dtype's contraction: bf16/fp16 = the measured bf16
+    figure; fp32 runs three TF32 products, TF32 = bf16 x 1/2 (the guide's nominal
+    dense ratio, 1.125 vs 2.25 PFLOP/s), so the fp32-accurate peak is bf16 / 6."""
+    b = peaks["bf16_tflops"]
+    return {"bf16": b, "fp16": b, "fp32": b / 2.0 / 3.0}[dtype]
 
 
 def main():
     a = parse()
+    if a.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(a, rank, world)
+        return
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(a))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if a.impl == "reference":
-        run_reference(a, rank, world)
-        return
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -217,13 +268,13 @@ def main():
     spec, m = canonical_spec(a.algo)
     algo = Wn.WinoAlgo(spec, m, lowering=a.lowering)
     tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[a.dtype]
-    from paper_1905_05233_b200 import distributed as D
-    nl = c["N"]                     # images per rank (weak scaling)
-    N = nl * world                  # global batch
-    # rank r draws its own images (seed r); the weights are the seed-0 weights on every rank
-    x64, _ = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=rank, xdist=c["xdist"])
-    _, w64 = datagen.layer(nl, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=0, xdist=c["xdist"])
-    x = torch.from_numpy(np.ascontiguousarray(x64)).to(tdt).cuda()
+    N = c["N"]                                      # the workload's (global) batch
+    lo, hi = rank_batch(N, world, rank, a.scaling)
+    nl = hi - lo                                    # images on this rank
+    n_job = nl * world                              # images processed by the whole job per step
+    # the global batch is drawn once from seed 0 (x first, then w); each rank keeps its slice
+    x64, w64 = datagen.layer(N, c["C"], c["K"], c["H"], c["W"], a.dtype, seed=0, xdist=c["xdist"])
+    x = torch.from_numpy(np.ascontiguousarray(x64[lo:hi])).to(tdt).cuda()
     if a.layout == "nhwc":
         x = x.permute(0, 2, 3, 1).contiguous()
     w = torch.from_numpy(w64).to(tdt).cuda()
@@ -232,52 +283,147 @@ def main():
     Ho, Wo = H, W
     y = torch.empty((nl, K, Ho, Wo) if a.layout == "nchw" else (nl, Ho, Wo, K), dtype=tdt, device="cuda")
     ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, nl, C, H, W, K, 1, a.dtype, a.layout))
-    st = torch.cuda.current_stream()
+    st = torch.cuda.Stream()          # a side stream (graph capture needs one), current for the whole run
+    torch.cuda.set_stream(st)
 
     def step():
         Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st, layout=a.layout)
         return Wn.wino_last_launch_count()
 
-    for _ in range(max(3, a.warmup)):
-        step()
+    with torch.cuda.stream(st):
+        for _ in range(max(3, a.warmup)):
+            per_step = step()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches = 0
+    graph = None
+    if a.graph == "on":
+        # the whole step (K2 fork/join on the library's side stream, K1, K3, K4) as one CUDA graph
+        try:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=st):
+                per_step = step()
+            torch.cuda.synchronize()
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 -- reported, then the eager loop is timed
+            graph = None
+            graph_err = f"{type(e).__name__}: {e}"[:200]
+
+    def timed(steps, use_graph):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for _ in range(steps):
+                if use_graph:
+                    graph.replay()
+                else:
+                    step()
+            e1.record(st)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = e0.elapsed_time(e1) / steps
+        if world > 1:
+            from paper_1905_05233_b200 import distributed as D
+            t = D.max_over_ranks(t, dist, "cuda")
+        return t
+
     with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        ev0.record(st)
-        for _ in range(a.steps):
-            launches += step()
-        ev1.record(st)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ms = ev0.elapsed_time(ev1) / a.steps
-    if world > 1:
-        ms = D.max_over_ranks(ms, dist, "cuda")
-    flops = direct_flops(N, C, K, Ho, Wo)
+        ms = timed(a.steps, graph is not None)
+    launches = per_step * a.steps
+    flops = direct_flops(n_job, C, K, Ho, Wo)
     value = flops / (ms * 1e-3) / 1e12
 
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": a.steps,
-           "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
            "config": {"workload": c["desc"], "algo": f"{a.algo} {{{spec}}} m={m} mu={algo.mu} ratio={algo.ratio_2d:.4g}",
-                      "lowering": a.lowering, "layout": a.layout, "global_batch": N, "per_gpu_batch": nl,
+                      "lowering": a.lowering, "layout": a.layout, "global_batch": n_job, "per_gpu_batch": nl,
                       "parallelism": f"dp{world} (batch-partitioned, no data-path collective)",
-                      "l2": "inputs larger than L2 (x %.0f MB, V and M staged through HBM)" % (
-                          x.numel() * x.element_size() / 1e6 * world)},
+                      "launch": "CUDA graph per step" if graph is not None else "eager",
+                      "l2": "inputs larger than L2 (x %.0f MB per GPU; V and M staged through HBM)" % (
+                          x.numel() * x.element_size() / 1e6)},
            "gpu_launches": launches, "clocks": clk.summary()}
+    if a.graph == "on" and graph is None:
+        out["config"]["graph_error"] = graph_err
     if not a.no_extras:
-        extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, c, spec)
+        out["ms_per_step_eager"] = timed(a.steps, False) if graph is not None else ms
+        extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, c, spec, graph, timed)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
 
 
-def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, c, spec):
+def layer_bytes(nl, C, K, H, W, es, g):
+    """Compulsory (x + w + y) and staged (+ U, V and the fp32 M written and read)
+    bytes of one layer on one GPU."""
+    pl = g["planes"]
+    xb, yb, wb = nl * C * H * W * es, nl * K * H * W * es, K * C * 9 * es
+    Ub = pl * g["S"] * K * g["Cp"] * es
+    Vb = pl * g["Q"] * g["T"] * g["Cp"] * es
+    Mb = g["Q"] * K * g["T"] * 4
+    return dict(x=xb, y=yb, w=wb, U=Ub, V=Vb, M=Mb, compulsory=xb + yb + wb, staged=xb + yb + wb + Ub + 2 * Vb + 2 * Mb)
+
+
+def kernel_rooflines(algo, dtype, x, w, y, ws, st, nl, C, K, H, W, reps, lay, peaks, peak_src, a):
+    """Per-kernel CUDA-event times and the roofline of the dominant kernel."""
+    import paper_1905_05233_b200 as Wn
+    g = Wn.geometry(algo, nl, C, H, W, K, 1, dtype)
+    es = 4 if dtype == "fp32" else 2
+    B = layer_bytes(nl, C, K, H, W, es, g)
+    gemm_flops = 2.0 * g["T"] * C * K * g["S"] * (3 if dtype == "fp32" else 1)   # fp32: 3 TF32 products
+    kern = per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dtype, reps, lay=lay)
+    hbm = peaks["hbm_gbs"] * 1e9
+    tc = tc_peak_tflops(dtype, peaks) * 1e12 * (3 if dtype == "fp32" else 1)      # raw TF32 rate for fp32
+    info = {
+        "weight_transform": {"bytes": B["w"] + B["U"], "flops": None},
+        "input_transform": {"bytes": B["x"] + B["V"], "flops": None},
+        "domain_gemm": {"bytes": B["V"] + B["U"] + B["M"], "flops": gemm_flops},
+        "output_transform": {"bytes": B["M"] + B["y"], "flops": None},
+    }
+    kernels = {}
+    for k_, ms_ in kern.items():
+        d = info[k_]
+        t_mem = d["bytes"] / hbm
+        t_tc = d["flops"] / tc if d["flops"] else 0.0
+        kernels[k_] = {"us": ms_ * 1e3, "algorithmic_bytes": d["bytes"], "GB/s": d["bytes"] / (ms_ * 1e-3) / 1e9,
+                       "TFLOP/s": (d["flops"] / (ms_ * 1e-3) / 1e12) if d["flops"] else None,
+                       "bound": "tensor" if t_tc > t_mem else "hbm", "frac": max(t_mem, t_tc) / (ms_ * 1e-3)}
+    dom = max(kernels, key=lambda k_: kernels[k_]["us"])
+    kd = kernels[dom]
+    if kd["bound"] == "tensor":
+        ach = info[dom]["flops"] / (kd["us"] * 1e-6) / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc / 1e12, "unit": "TFLOP/s",
+                "frac": ach / (tc / 1e12), "traffic": ncu_traffic(dom, a, dtype), "peak_source": peak_src}
+    else:
+        ach = info[dom]["bytes"] / (kd["us"] * 1e-6) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": ncu_traffic(dom, a, dtype), "peak_source": peak_src}
+    if dtype == "fp32":
+        roof["tf32_peak_note"] = ("3xTF32 (hi*hi + hi*lo + lo*hi); TF32 dense peak = measured bf16 %.1f TFLOP/s x 1/2 "
+                                  "(nominal ratio 1.125/2.25 PFLOP/s); fp32-accurate peak = that / 3" % peaks["bf16_tflops"])
+    return kernels, roof, B, gemm_flops
+
+
+def layer_fracs(ms, B, gemm_flops, dtype, peaks, sustained=False):
+    """North-star layer rooflines: compulsory bytes (the fused ideal) and staged
+    bytes (this K1 -> K3 -> K4 design) against the dtype's tensor peak."""
+    hbm = peaks["hbm_gbs"] * 1e9
+    tcp = tc_peak_tflops(dtype, peaks) * 1e12
+    if sustained:
+        tcp *= peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) / peaks["bf16_tflops"]
+    f = gemm_flops / (3 if dtype == "fp32" else 1)                  # fp32-accurate flops at the fp32-accurate peak
+    t_roof = max(f / tcp, B["compulsory"] / hbm)
+    t_staged = max(f / tcp, B["staged"] / hbm)
+    return {"t_roof_us": t_roof * 1e6, "frac_compulsory": t_roof / (ms * 1e-3), "t_staged_us": t_staged * 1e6,
+            "frac_staged": t_staged / (ms * 1e-3), "tensor_peak_tflops": tcp / 1e12}
+
+
+def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, c, spec, graph, timed):
     import torch
     import paper_1905_05233_b200 as Wn
     peaks, peak_src = load_peaks()
@@ -290,69 +436,73 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
     if world > 1:
         from paper_1905_05233_b200 import distributed as D
         stats = D.reduce_stats(stats, dist)
-    out["accuracy"] = {k: (float(v) if not isinstance(v, int) else v) for k, v in Wn.summary(stats.cpu()).items()}
+    s = stats.cpu()
+    out["accuracy"] = {k: (float(v) if not isinstance(v, int) else v) for k, v in Wn.summary(s).items()}
+    out["accuracy"]["stats8"] = [float(v) for v in s.tolist()]
     del yref
-    # ---------------------------------------------------------------- per-kernel breakdown (same stream, events)
-    g = Wn.geometry(algo, nl, C, H, W, K, 1, a.dtype)
-    es = 4 if a.dtype == "fp32" else 2
-    pl = g["planes"]
-    U = ws[:0]
-    base = ws.data_ptr()
-    kern = per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, a.dtype, max(20, a.steps // 4),
-                            lay=0 if a.layout == "nchw" else 1)
-    T_, Q, S, Cp, Tp = g["T"], g["Q"], g["S"], g["Cp"], g["Tp"]
-    xb = x.numel() * x.element_size()
-    yb = y.numel() * y.element_size()
-    wb = w.numel() * w.element_size()
-    Ub = pl * S * K * Cp * es
-    Vb = pl * Q * T_ * Cp * es
-    Mb = Q * K * T_ * 4
-    gemm_flops = 2.0 * T_ * C * K * S * (3 if a.dtype == "fp32" else 1)
-    hbm = peaks["hbm_gbs"] * 1e9
-    tc_peak = peaks["bf16_tflops"] * 1e12 * (0.5 if a.dtype == "fp32" else 1.0)   # tf32 = bf16 / 2 (nominal ratio)
-    info = {
-        "weight_transform": {"bytes": wb + Ub, "flops": None},
-        "input_transform": {"bytes": xb + Vb, "flops": None},
-        "domain_gemm": {"bytes": Vb + Ub + Mb, "flops": gemm_flops},
-        "output_transform": {"bytes": Mb + yb, "flops": None},
-    }
-    kernels = {}
-    for k_, ms_ in kern.items():
-        d = info[k_]
-        t_mem = d["bytes"] / hbm
-        t_tc = d["flops"] / tc_peak if d["flops"] else 0.0
-        kernels[k_] = {"us": ms_ * 1e3, "algorithmic_bytes": d["bytes"], "GB/s": d["bytes"] / (ms_ * 1e-3) / 1e9,
-                       "TFLOP/s": (d["flops"] / (ms_ * 1e-3) / 1e12) if d["flops"] else None,
-                       "bound": "tensor" if t_tc > t_mem else "hbm", "frac": max(t_mem, t_tc) / (ms_ * 1e-3)}
+    # ---------------------------------------------------------------- per-kernel breakdown + roofline
+    lay = 0 if a.layout == "nchw" else 1
+    kernels, roof, B, gemm_flops = kernel_rooflines(algo, a.dtype, x, w, y, ws, st, nl, C, K, H, W,
+                                                    max(20, a.steps // 4), lay, peaks, peak_src, a)
     out["kernels"] = kernels
-    dom = max(kernels, key=lambda k_: kernels[k_]["us"])
-    kd = kernels[dom]
-    if kd["bound"] == "tensor":
-        ach = info[dom]["flops"] / (kd["us"] * 1e-6) / 1e12
-        out["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc_peak / 1e12,
-                           "unit": "TFLOP/s", "frac": ach / (tc_peak / 1e12), "traffic": ncu_traffic(dom, a),
-                           "peak_source": peak_src}
-    else:
-        ach = info[dom]["bytes"] / (kd["us"] * 1e-6) / 1e9
-        out["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
-                           "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": ncu_traffic(dom, a),
-                           "peak_source": peak_src}
-    # ---------------------------------------------------------------- layer-level rooflines (north star)
+    out["roofline"] = roof
     ms = out["ms_per_step"]
-    # per GPU (every rank runs the same per-GPU layer concurrently)
-    comp_bytes = xb + yb + wb
-    t_roof = max(gemm_flops / tc_peak, comp_bytes / hbm)
-    t_staged = max(gemm_flops / tc_peak, (comp_bytes + Ub + 2 * Vb + 2 * Mb) / hbm)
-    out["layer_roofline"] = {"t_roof_us": t_roof * 1e6, "frac_compulsory": t_roof / (ms * 1e-3),
-                             "t_staged_us": t_staged * 1e6, "frac_staged": t_staged / (ms * 1e-3),
-                             "peaks": peak_src}
+    out["layer_roofline"] = dict(layer_fracs(ms, B, gemm_flops, a.dtype, peaks), peaks=peak_src)
+    # ---------------------------------------------------------------- sustained (long loop, power cap)
+    if world == 1 and graph is not None:
+        steps_s = max(200, int(2000.0 / max(ms, 1e-3)))   # ~2 s of back-to-back steps
+        ms_s = timed(steps_s, True)
+        out["sustained"] = {"steps": steps_s, "ms_per_step": ms_s,
+                            "value": direct_flops(nl, C, K, H, W) / (ms_s * 1e-3) / 1e12,
+                            "layer_roofline": layer_fracs(ms_s, B, gemm_flops, a.dtype, peaks, sustained=True)}
+    # ---------------------------------------------------------------- the other dtypes (same workload, rank 0 slice)
+    if world == 1 and a.workload == "cfg5" and not a.no_dtypes:
+        out["rooflines_by_dtype"] = {a.dtype: {"roofline": roof, "layer_roofline": out["layer_roofline"],
+                                               "ms_per_step": ms}}
+        for dt in ("bf16", "fp16", "fp32"):
+            if dt != a.dtype:
+                out["rooflines_by_dtype"][dt] = dtype_roofline(a, algo, dt, c, st, peaks, peak_src)
     # ---------------------------------------------------------------- end to end (host buffers)
     out["e2e"] = e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist)
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
     if world == 1:
         out["cpu_baseline"] = cpu_baseline(a.algo, a.dtype, c)
     if world == 1 and (a.sweep == "on" or (a.sweep == "auto" and a.workload == "cfg5")):
-        out["sweep"] = sweep(c, st)
+        out["sweep"] = sweep(c, st, peaks)
+
+
+def dtype_roofline(a, algo, dt, c, st, peaks, peak_src):
+    """Step time, dominant-kernel roofline and layer fractions of the workload in
+    another dtype (same algorithm)."""
+    import numpy as np
+    import torch
+    import datagen
+    import paper_1905_05233_b200 as Wn
+    tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[dt]
+    N, C, K, H, W = c["N"], c["C"], c["K"], c["H"], c["W"]
+    x64, w64 = datagen.layer(N, C, K, H, W, dt, seed=0, xdist=c["xdist"])
+    x = torch.from_numpy(x64).to(tdt).cuda()
+    w = torch.from_numpy(w64).to(tdt).cuda()
+    del x64
+    y = torch.empty((N, K, H, W), dtype=tdt, device="cuda")
+    ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, N, C, H, W, K, 1, dt))
+    with torch.cuda.stream(st):
+        for _ in range(3):
+            Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(20):
+            Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st)
+        e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 20
+    kernels, roof, B, gemm_flops = kernel_rooflines(algo, dt, x, w, y, ws, st, N, C, K, H, W, 20, 0, peaks,
+                                                    peak_src, a)
+    del x, w, y, ws
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "value": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12, "kernels": kernels,
+            "roofline": roof, "layer_roofline": layer_fracs(ms, B, gemm_flops, dt, peaks)}
 
 
 def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps, lay=0):
@@ -365,7 +515,7 @@ def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps, lay=0):
     U = ws.data_ptr()
     nbU = g["planes"] * g["S"] * K * g["Cp"] * es
     V = U + ((nbU + 1023) // 1024) * 1024
-    nbV = g["planes"] * g["Q"] * g["T"] * g["Cp"] * es
+    nbV = g["planes"] * g["Q"] * g["TB"] * 128 * g["Cp"] * es   # V is padded to whole 128-tile blocks
     M = V + ((nbV + 1023) // 1024) * 1024
     L = lib()
     s = ctypes.c_void_p(st.cuda_stream)
@@ -402,14 +552,17 @@ def e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist):
     xh.copy_(x.cpu())
     yh = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
     steps = max(5, min(a.steps, 30))
-    for _ in range(2):
-        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for _ in range(steps):
-        Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
-    e1.record(st)
+    with torch.cuda.stream(st):
+        for _ in range(2):
+            Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            Wn.wino_conv2d_host_io(xh, x, w, algo, y, yh, ws, stream=st, layout=a.layout)
+        e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / steps
     if world > 1:
@@ -422,8 +575,10 @@ def e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist):
             "path": "wino_conv2d_host_io: pinned x -> device, layer, device y -> pinned host"}
 
 
-def sweep(c, st):
-    """Tile-size / polynomial-set sweep of cfg5 (BASELINE configs[4]) on one GPU."""
+def sweep(c, st, peaks):
+    """Tile-size / polynomial-set sweep of cfg5 (BASELINE configs[4]) on one GPU,
+    m = 2..8 with linear (Toom-Cook) and one-quadratic (a^2+1) sets; each row
+    carries its own layer roofline fractions."""
     import numpy as np
     import torch
     import datagen
@@ -438,7 +593,8 @@ def sweep(c, st):
         w = torch.from_numpy(w64).to(tdt).cuda()
         del x64
         yref = Wn.wino_direct_conv2d_f64(x, w, 1, stream=st)
-        for name in ("lin2", "sup1_2", "lin3", "lin4", "sup1_4", "lin6", "sup1_6", "lin8", "sup1_8"):
+        for name in ("lin2", "sup1_2", "lin3", "sup1_3", "lin4", "sup1_4", "lin5", "sup1_5", "lin6", "sup1_6", "lin7",
+                     "sup1_7", "lin8", "sup1_8"):
             spec, m = canonical_spec(name)
             algo = Wn.WinoAlgo(spec, m)
             y = torch.empty((N, K, H, W), dtype=tdt, device="cuda")
@@ -454,8 +610,12 @@ def sweep(c, st):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 10
             s = Wn.summary(Wn.wino_error_stats(y, yref, m, stream=st).cpu())
+            g = Wn.geometry(algo, N, C, H, W, K, 1, dt)
+            B = layer_bytes(N, C, K, H, W, 4 if dt == "fp32" else 2, g)
+            fr = layer_fracs(ms, B, 2.0 * g["T"] * C * K * g["S"] * (3 if dt == "fp32" else 1), dt, peaks)
             rows.append({"algo": name, "dtype": dt, "mu": algo.mu, "ratio": round(algo.ratio_2d, 4), "ms": ms,
                          "tflops_direct_eq": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12,
+                         "frac_compulsory": fr["frac_compulsory"], "frac_staged": fr["frac_staged"],
                          "rel_l1": s["rel_l1"], "mean_rel": s["mean_rel"], "nonfinite": s["nonfinite"]})
             del ws, y
         del x, w, yref
@@ -463,7 +623,7 @@ def sweep(c, st):
     return rows
 
 
-def ncu_traffic(kernel, a):
+def ncu_traffic(kernel, a, dtype=None):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary, if one
     matches this workload (profiles/ncu_full_*.json), else None."""
     import glob
@@ -471,7 +631,7 @@ def ncu_traffic(kernel, a):
         try:
             with open(p) as f:
                 d = json.load(f)
-            e = d.get(f"{a.workload}/{a.algo}/{a.dtype}/{kernel}")
+            e = d.get(f"{a.workload}/{a.algo}/{dtype or a.dtype}/{kernel}")
             if e:
                 return e.get("dram_bytes")
         except Exception:

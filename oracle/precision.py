@@ -290,15 +290,37 @@ def pipeline_conv1d(ts, x, h, dtype, bf16_mode="rne"):
     return rd(dtype, AT @ p, bf16_mode).T
 
 
-def paper_conv2d_tiles(ts, d, g, dtype, bf16_mode="rne"):
+def pairwise_sum(terms, add):
+    """Pairwise (tree) summation over channels, one of the accuracy boosters
+    P:611 lists as composable with the method ("pairwise summation over
+    channels"): sum(t[0:n]) = add(sum(t[0:h]), sum(t[h:n])) with h the largest
+    power of two below n -- the same tree as combining adjacent pairs level by
+    level and carrying an odd last element up unchanged."""
+    n = len(terms)
+    if n == 1:
+        return terms[0]
+    h = 1
+    while 2 * h < n:
+        h *= 2
+    return add(pairwise_sum(terms[:h], add), pairwise_sum(terms[h:], add))
+
+
+def paper_conv2d_tiles(ts, d, g, dtype, bf16_mode="rne", csum="sequential", acc="dtype"):
     """PAPER mode on a batch of single-channel-summed tile samples:
     d[C, S, n_x, n_x], g[C, S, 3, 3] -> Y[S, m, m].  Kernel transform rows then
     columns, input transform rows then columns, product, channel sum in the
-    Winograd domain (ascending c), output transform rows then columns."""
+    Winograd domain, output transform rows then columns; every op per P:556.
+
+    Channel sum variants (composable accuracy boosters; readings M1, M2 in
+    DESIGN.md): csum = "sequential" (ascending c, the paper's baseline) or
+    "pairwise" (pairwise_sum); acc = "dtype" (every partial sum cast to the
+    dtype) or "fp32" (mixed precision: the rounded products P_c are accumulated
+    in fp32 and the channel sum is cast to the dtype once, before the output
+    transform)."""
     G, BT, AT = paper_matrices(ts, dtype, bf16_mode)
     d = np.asarray(d, np.float32)
     g = np.asarray(g, np.float32)
-    Msum = None
+    prods = []
     for c in range(d.shape[0]):
         gc = g[c].transpose(1, 2, 0)                                  # (3, 3, S)
         dc = d[c].transpose(1, 2, 0)                                  # (nx, nx, S)
@@ -307,8 +329,28 @@ def paper_conv2d_tiles(ts, d, g, dtype, bf16_mode="rne"):
         V = po_matmul(BT, dc, dtype, bf16_mode)
         V = po_matmul(BT, V.transpose(1, 0, 2), dtype, bf16_mode).transpose(1, 0, 2)
         with np.errstate(over="ignore", invalid="ignore"):
-            P = rd(dtype, (U * V).astype(np.float32), bf16_mode)
-            Msum = P if Msum is None else rd(dtype, (Msum + P).astype(np.float32), bf16_mode)
+            prods.append(rd(dtype, (U * V).astype(np.float32), bf16_mode))
+    if acc == "dtype":
+        def add(a, b):
+            with np.errstate(over="ignore", invalid="ignore"):
+                return rd(dtype, (a + b).astype(np.float32), bf16_mode)
+    elif acc == "fp32":
+        def add(a, b):
+            with np.errstate(over="ignore", invalid="ignore"):
+                return (a + b).astype(np.float32)
+    else:
+        raise ValueError(acc)
+    if csum == "sequential":
+        Msum = prods[0]
+        for P_c in prods[1:]:
+            Msum = add(Msum, P_c)
+    elif csum == "pairwise":
+        Msum = pairwise_sum(prods, add)
+    else:
+        raise ValueError(csum)
+    if acc == "fp32":
+        with np.errstate(over="ignore"):
+            Msum = rd(dtype, Msum, bf16_mode)
     Y = po_matmul(AT, Msum, dtype, bf16_mode)
     Y = po_matmul(AT, Y.transpose(1, 0, 2), dtype, bf16_mode).transpose(1, 0, 2)
     return Y.transpose(2, 0, 1)

@@ -23,9 +23,30 @@ def _dt(t):
         raise WinoError(1, f"unsupported dtype {t.dtype}")
 
 
-def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream(stream=None, device=None):
+    """The stream the library launches on: `stream`, else the current stream of
+    `device` (the tensors' device, not whichever device happens to be current)."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _on_stream(stream, *tensors):
+    """Allocations made on the current stream but used on another `stream` must
+    not be recycled by the caching allocator before that stream's kernels ran."""
+    if stream is None:
+        return
+    cur = torch.cuda.current_stream(stream.device)
+    if stream.cuda_stream != cur.cuda_stream:
+        for t in tensors:
+            if t is not None and t.is_cuda:
+                t.record_stream(stream)
+
+
+def _check_out(out, shape, dtype, device):
+    if tuple(out.shape) != tuple(shape) or out.dtype != dtype or out.device != device or not out.is_contiguous():
+        raise WinoError(1, f"out must be a contiguous {dtype} tensor of shape {tuple(shape)} on {device}; "
+                           f"got {out.dtype} {tuple(out.shape)} on {out.device}"
+                           f"{'' if out.is_contiguous() else ' (non-contiguous)'}")
 
 
 def _ptr(t):
@@ -129,7 +150,8 @@ def alloc_workspace(nbytes, device="cuda"):
 def wino_conv2d(x, w, algo, pad=1, layout="nchw", out=None, workspace=None, stream=None):
     """y = conv(x, w) (valid cross-correlation, stride 1, zero padding `pad`)
     through libwino's kernels.  x: [N,C,H,W] ("nchw") or [N,H,W,C] ("nhwc"),
-    w: [K,C,3,3], same dtype, CUDA; y in the layout of x."""
+    w: [K,C,3,3], same dtype, same CUDA device; y in the layout of x.  Runs on
+    `stream` (default: the current stream of x's device)."""
     if layout == "nchw":
         N, C, H, W = x.shape
     elif layout == "nhwc":
@@ -137,19 +159,30 @@ def wino_conv2d(x, w, algo, pad=1, layout="nchw", out=None, workspace=None, stre
     else:
         raise WinoError(1, f"bad layout {layout!r}")
     K = w.shape[0]
-    assert w.shape == (K, C, 3, 3) and w.dtype == x.dtype and x.is_cuda and w.is_cuda
-    x = x.contiguous()
-    w = w.contiguous()
+    if not (x.is_cuda and w.is_cuda and x.device == w.device):
+        raise WinoError(1, "x and w must be CUDA tensors on the same device")
+    if tuple(w.shape) != (K, C, 3, 3) or w.dtype != x.dtype:
+        raise WinoError(1, f"w must be [{K},{C},3,3] of dtype {x.dtype}; got {tuple(w.shape)} {w.dtype}")
+    dt = _TORCH_DT.get(x.dtype)
+    if dt is None:
+        raise WinoError(1, f"unsupported dtype {x.dtype}")
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
-    if out is None:
-        shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
-        out = torch.empty(shape, dtype=x.dtype, device=x.device)
-    dt = _TORCH_DT[x.dtype]
-    nbytes = wino_conv2d_workspace(algo, N, C, H, W, K, pad, dt, layout)
-    if workspace is None:
-        workspace = alloc_workspace(nbytes, x.device)
-    check(lib().wino_conv2d(_ptr(x), _ptr(w), N, C, H, W, K, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
-                            _ptr(out), _ptr(workspace), workspace.numel(), _stream(stream)))
+    shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
+    with torch.cuda.device(x.device):
+        x = x.contiguous()
+        w = w.contiguous()
+        if out is None:
+            out = torch.empty(shape, dtype=x.dtype, device=x.device)
+        else:
+            _check_out(out, shape, x.dtype, x.device)
+        nbytes = wino_conv2d_workspace(algo, N, C, H, W, K, pad, dt, layout)
+        if workspace is None:
+            workspace = alloc_workspace(nbytes, x.device)
+        elif workspace.device != x.device or workspace.numel() < nbytes:
+            raise WinoError(6, f"workspace must hold {nbytes} bytes on {x.device}")
+        _on_stream(stream, x, w, out, workspace)
+        check(lib().wino_conv2d(_ptr(x), _ptr(w), N, C, H, W, K, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
+                                _ptr(out), _ptr(workspace), workspace.numel(), _stream(stream, x.device)))
     return out
 
 
@@ -161,9 +194,21 @@ def wino_conv2d_host_io(x_host, x_dev, w, algo, out_dev, out_host, workspace, pa
         N, H, W, C = x_dev.shape
     K = w.shape[0]
     dt = _TORCH_DT[x_dev.dtype]
-    check(lib().wino_conv2d_host_io(_ptr(x_host), _ptr(x_dev), _ptr(w), N, C, H, W, K, pad, algo.handle,
-                                    DTYPES[dt], LAYOUTS[layout], _ptr(out_dev), _ptr(out_host), _ptr(workspace),
-                                    workspace.numel(), _stream(stream)))
+    Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
+    shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
+    if x_host.is_cuda or out_host.is_cuda or not (x_host.is_pinned() and out_host.is_pinned()):
+        raise WinoError(1, "x_host and out_host must be pinned host tensors")
+    if x_host.numel() * x_host.element_size() != x_dev.numel() * x_dev.element_size() or not x_host.is_contiguous():
+        raise WinoError(1, "x_host must be a contiguous host copy of x_dev's shape and dtype")
+    if out_host.numel() * out_host.element_size() != out_dev.numel() * out_dev.element_size() \
+            or not out_host.is_contiguous():
+        raise WinoError(1, "out_host must be a contiguous host buffer of out_dev's size")
+    _check_out(out_dev, shape, x_dev.dtype, x_dev.device)
+    with torch.cuda.device(x_dev.device):
+        _on_stream(stream, x_dev, w, out_dev, workspace)
+        check(lib().wino_conv2d_host_io(_ptr(x_host), _ptr(x_dev), _ptr(w), N, C, H, W, K, pad, algo.handle,
+                                        DTYPES[dt], LAYOUTS[layout], _ptr(out_dev), _ptr(out_host),
+                                        _ptr(workspace), workspace.numel(), _stream(stream, x_dev.device)))
 
 
 def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
@@ -199,7 +244,9 @@ def wino_weight_transform(w, algo, stream=None):
     dt = _TORCH_DT[w.dtype]
     g = geometry(algo, 1, C, 3, 3, K, 1, dt)
     U = torch.empty((g["planes"], g["S"], K, g["Cp"]), dtype=w.dtype, device=w.device)
-    check(lib().wino_weight_transform(_ptr(w.contiguous()), K, C, algo.handle, DTYPES[dt], _ptr(U), _stream(stream)))
+    with torch.cuda.device(w.device):
+        check(lib().wino_weight_transform(_ptr(w.contiguous()), K, C, algo.handle, DTYPES[dt], _ptr(U),
+                                          _stream(stream, w.device)))
     return U
 
 
@@ -214,8 +261,9 @@ def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
     g = geometry(algo, N, C, H, W, 1, pad, dt)
     V = torch.empty((g["planes"], g["TB"], g["Cp"] // g["CBW"], g["Q"], 128, g["CBW"]), dtype=x.dtype,
                     device=x.device)
-    check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
-                                     _ptr(V), _stream(stream)))
+    with torch.cuda.device(x.device):
+        check(lib().wino_input_transform(_ptr(x.contiguous()), N, C, H, W, pad, algo.handle, DTYPES[dt], LAYOUTS[layout],
+                                         _ptr(V), _stream(stream, x.device)))
     return V
 
 
@@ -224,7 +272,8 @@ def wino_domain_gemm(V, U, algo, C, K, T, stream=None):
     dt = _TORCH_DT[V.dtype]
     Tp = -(-T // 32) * 32
     M = torch.empty((algo.domain ** 2, K, Tp), dtype=torch.float32, device=V.device)
-    check(lib().wino_domain_gemm(_ptr(V), _ptr(U), T, C, K, algo.handle, DTYPES[dt], _ptr(M), _stream(stream)))
+    with torch.cuda.device(V.device):
+        check(lib().wino_domain_gemm(_ptr(V), _ptr(U), T, C, K, algo.handle, DTYPES[dt], _ptr(M), _stream(stream, V.device)))
     return M
 
 
@@ -232,8 +281,9 @@ def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None,
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
     shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
     y = torch.empty(shape, dtype=TORCH_OF[dtype], device=M.device)
-    check(lib().wino_output_transform(_ptr(M), N, K, H, W, pad, algo.handle, DTYPES[dtype], LAYOUTS[layout],
-                                      _ptr(y), _stream(stream)))
+    with torch.cuda.device(M.device):
+        check(lib().wino_output_transform(_ptr(M), N, K, H, W, pad, algo.handle, DTYPES[dtype], LAYOUTS[layout],
+                                          _ptr(y), _stream(stream, M.device)))
     return y
 
 
@@ -244,8 +294,24 @@ def wino_conv1d_tiles(x, h, algo, per_op_rounding=True, stream=None):
     T = x.shape[0]
     assert x.shape == (T, algo.m + 2) and h.shape == (T, 3) and x.dtype == h.dtype
     y = torch.empty((T, algo.m), dtype=x.dtype, device=x.device)
-    check(lib().wino_conv1d_tiles(_ptr(x.contiguous()), _ptr(h.contiguous()), T, algo.handle, _dt(x),
-                                  1 if per_op_rounding else 0, _ptr(y), _stream(stream)))
+    with torch.cuda.device(x.device):
+        check(lib().wino_conv1d_tiles(_ptr(x.contiguous()), _ptr(h.contiguous()), T, algo.handle, _dt(x),
+                                      1 if per_op_rounding else 0, _ptr(y), _stream(stream, x.device)))
+    return y
+
+
+def wino_conv2d_tiles_paper(d, g, algo, csum="sequential", acc="dtype", stream=None):
+    """Paper-mode multi-channel 2D tiles: d [C][S][m+2][m+2], g [C][S][3][3] ->
+    Y [S][m][m] (include/wino.h wino_conv2d_tiles_paper)."""
+    C, S = d.shape[:2]
+    nx = algo.m + 2
+    if tuple(d.shape) != (C, S, nx, nx) or tuple(g.shape) != (C, S, 3, 3) or d.dtype != g.dtype:
+        raise WinoError(1, "d must be [C][S][m+2][m+2] and g [C][S][3][3] of one dtype")
+    y = torch.empty((S, algo.m, algo.m), dtype=d.dtype, device=d.device)
+    with torch.cuda.device(d.device):
+        check(lib().wino_conv2d_tiles_paper(_ptr(d.contiguous()), _ptr(g.contiguous()), C, S, algo.handle, _dt(d),
+                                            {"sequential": 0, "pairwise": 1}[csum], {"dtype": 0, "fp32": 1}[acc],
+                                            _ptr(y), _stream(stream, d.device)))
     return y
 
 
@@ -256,8 +322,9 @@ def wino_error_stats(y, y_ref, m, stream=None):
     stats = torch.empty(8, dtype=torch.float64, device=y.device)
     nbytes = lib().wino_error_stats_scratch(N, K, Ho, Wo, m)
     scratch = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=y.device)
-    check(lib().wino_error_stats(_ptr(y.contiguous()), _dt(y), _ptr(y_ref.contiguous()), N, K, Ho, Wo, m,
-                                 _ptr(stats), _ptr(scratch), _stream(stream)))
+    with torch.cuda.device(y.device):
+        check(lib().wino_error_stats(_ptr(y.contiguous()), _dt(y), _ptr(y_ref.contiguous()), N, K, Ho, Wo, m,
+                                     _ptr(stats), _ptr(scratch), _stream(stream, y.device)))
     return stats
 
 
@@ -265,8 +332,9 @@ def wino_direct_conv2d_f64(x, w, pad=1, stream=None):
     N, C, H, W = x.shape
     K = w.shape[0]
     y = torch.empty((N, K, H + 2 * pad - 2, W + 2 * pad - 2), dtype=torch.float64, device=x.device)
-    check(lib().wino_direct_conv2d_f64(_ptr(x.contiguous()), _ptr(w.contiguous()), N, C, H, W, K, pad, _dt(x),
-                                       _ptr(y), _stream(stream)))
+    with torch.cuda.device(x.device):
+        check(lib().wino_direct_conv2d_f64(_ptr(x.contiguous()), _ptr(w.contiguous()), N, C, H, W, K, pad, _dt(x),
+                                           _ptr(y), _stream(stream, x.device)))
     return y
 
 

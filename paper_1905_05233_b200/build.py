@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libwino.so")
 SOURCES = ["capi_host.cpp", "generator.cpp", "transforms.cu", "xform_f32.cu", "xform_f16.cu", "xform_bf16.cu",
-           "gemm.cu", "conv.cu", "misc.cu"]
+           "gemm.cu", "split.cu", "conv.cu", "misc.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

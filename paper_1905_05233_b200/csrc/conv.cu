@@ -14,8 +14,8 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
                                 wino_dtype dt, wino_layout layout, void* V, cudaStream_t st);
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
                             float* M, cudaStream_t st, int mb0 = 0, int nT = -1);
-wino_status run_domain_gemm_fused(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
-                                  float* M, void* y, int* done, cudaStream_t st);
+wino_status run_domain_gemm_split(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
+                                  float* M, void* y, int* cnt, cudaStream_t st);
 wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
                                  wino_dtype dt, wino_layout layout, void* y, cudaStream_t st, int t0 = 0,
                                  int nT = -1, int Tpm = 0, int disc = 0);
@@ -89,14 +89,10 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   // K2 (weights) and K1 (inputs) are independent: K2 runs on a library-owned
   // side stream forked from and joined back into the caller's stream (events,
   // so the pair stays CUDA-graph capturable), overlapping K1's start.
-  static thread_local cudaStream_t s_side = nullptr;
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (!s_side) {
-    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_side, cudaStreamNonBlocking));
-    WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-  }
-  cudaStream_t s_w = s_side;
+  DevState* ds = dev_state();   // per (thread, device): the caller's stream must be on the current device
+  if (!ds) return WINO_E_CUDA;
+  cudaEvent_t ev_fork = ds->fork, ev_join = ds->join;
+  cudaStream_t s_w = ds->side;
   WINO_CUDA_CHECK(cudaEventRecord(ev_fork, st));
   WINO_CUDA_CHECK(cudaStreamWaitEvent(s_w, ev_fork, 0));
   if ((s = run_weight_transform(w, K, C, al, dt, U, s_w)) != WINO_OK) return s;
@@ -104,7 +100,7 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   if ((s = run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, st)) != WINO_OK) return s;
   WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev_join, 0));
   if (layout == WINO_NCHW && !fused_disabled()) {
-    s = run_domain_gemm_fused(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
+    s = run_domain_gemm_split(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
     if (s != WINO_E_UNSUPPORTED) return s;   // OK or a real failure
   }
   const int cb = chunk_blocks(g, layout);
@@ -169,14 +165,10 @@ wino_status wino_conv2d_host_io(const void* x_host, void* x_dev, const void* w_d
       for (int j = nt - 1; j >= 0; --j) plan[nch++] = tail[j];
     }
   }
-  static thread_local cudaStream_t s_in = nullptr, s_out = nullptr;
-  static thread_local cudaEvent_t ev[2][64];
-  if (!s_in) {
-    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
-    WINO_CUDA_CHECK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
-    for (int a = 0; a < 2; ++a)
-      for (int j = 0; j < 64; ++j) WINO_CUDA_CHECK(cudaEventCreateWithFlags(&ev[a][j], cudaEventDisableTiming));
-  }
+  DevState* ds = dev_state();
+  if (!ds) return WINO_E_CUDA;
+  cudaStream_t s_in = ds->io_in, s_out = ds->io_out;
+  cudaEvent_t(&ev)[2][64] = ds->io_ev;
   // copies must not start before work already queued on the caller's stream
   cudaEvent_t start = ev[1][63];
   WINO_CUDA_CHECK(cudaEventRecord(start, st));

@@ -254,10 +254,18 @@ __device__ __forceinline__ void discard_l2(const void* p) {
 
 }  // namespace wino
 
-// Launch bookkeeping (misc.cu).
+// Launch bookkeeping and per-device library state (misc.cu).
 namespace wino {
 void count_launch(int n = 1);
 void reset_launch_count();
+struct DevState {
+  bool ready = false;
+  int sms = 0;
+  cudaStream_t side = nullptr, io_in = nullptr, io_out = nullptr;   // K2 fork; host_io copy streams
+  cudaEvent_t fork = nullptr, join = nullptr, io_ev[2][64] = {};
+};
+DevState* dev_state();   // of the calling thread's current device; nullptr (+ last error) on failure
+int num_sms();           // of the current device
 }  // namespace wino
 
 #define WINO_CUDA_CHECK(expr)                                                              \

@@ -49,7 +49,8 @@ inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int 
   g.TB = (g.T + 127) / 128;
   g.CBW = (int)(128 / g.es);
   size_t v_bytes = g.planes * (size_t)g.Q * g.TB * 128 * g.Cp * g.es;
-  size_t m_bytes = (size_t)g.Q * K * g.Tp * 4;
+  // M: [Q][K][Tp] for the staged K3 -> K4 pair, [TB][K][Q][128] for the fused split kernel
+  size_t m_bytes = (size_t)g.Q * K * g.TB * 128 * 4;
   g.offU = 0;
   g.offV = align_up(g.offU + u_bytes, 1024);
   g.offM = align_up(g.offV + v_bytes, 1024);

@@ -11,6 +11,42 @@ static thread_local int g_launches = 0;
 void count_launch(int n) { g_launches += n; }
 void reset_launch_count() { g_launches = 0; }
 
+// Library-owned streams / events and the SM count, per (host thread, device):
+// a thread that drives several GPUs gets each device's own objects.
+DevState* dev_state() {
+  constexpr int kMaxDev = 64;
+  static thread_local DevState st[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) {
+    set_last_error("dev_state: no current CUDA device");
+    return nullptr;
+  }
+  DevState& d = st[dev];
+  if (!d.ready) {
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d.io_in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&d.io_out, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
+    for (int a = 0; a < 2 && e == cudaSuccess; ++a)
+      for (int j = 0; j < 64 && e == cudaSuccess; ++j) e = cudaEventCreateWithFlags(&d.io_ev[a][j], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) {
+      set_last_error(std::string("dev_state: ") + cudaGetErrorString(e));
+      return nullptr;
+    }
+    if (d.sms <= 0) d.sms = 148;
+    d.ready = true;
+  }
+  return &d;
+}
+
+int num_sms() {
+  DevState* d = dev_state();
+  return d ? d->sms : 148;
+}
+
 // ------------------------------------------------------------------ K5: 1D tiles
 // y = A^T [(G h) (.) (B^T x)] per tile.  PAPER=true: every
 // scalar multiply/add in fp32 without contraction (__fmul_rn / __fadd_rn), cast
@@ -86,6 +122,123 @@ using C1Fn = void (*)(const C1Args&);
 static const C1Fn kC1[2][3][7][3] = {
     {C1TAB(WINO_F32, false), C1TAB(WINO_F16, false), C1TAB(WINO_BF16, false)},
     {C1TAB(WINO_F32, true), C1TAB(WINO_F16, true), C1TAB(WINO_BF16, true)}};
+
+// ------------------------------------------------------------------ K7: 2D tiles, paper mode
+// Multi-channel 2D Winograd of independent tile samples in PAPER mode,
+// the operation order of the oracle's paper_conv2d_tiles: for each channel c
+//   U = G g G^T  (rows then columns),  V = B^T d B  (rows then columns),
+//   P_c = rd(U (.) V),
+// every product and partial sum computed in fp32 without contraction and cast to
+// the dtype, matrix entries cast once; then the channel sum in the Winograd
+// domain and Y = A^T M A (rows then columns), per op.  Channel sum (P:611
+// boosters): csum 0 sequential (ascending c) / 1 pairwise (tree: the largest
+// power of two below n on the left); acc 0 every partial sum cast to the dtype /
+// 1 fp32 accumulation cast once (mixed precision).  Block = one sample, thread =
+// one Winograd point (i, j); the pairwise tree is a binary counter of partial
+// sums (an element at level l merges with the stored partial of level l).
+template <int DT, int M, int MU>
+__global__ void __launch_bounds__(256) conv2d_tiles_paper_kernel(const typename DType<DT>::T* __restrict__ d,
+                                                                 const typename DType<DT>::T* __restrict__ g, int C,
+                                                                 int64_t S, const __grid_constant__ XformParams xp,
+                                                                 int csum, int acc32,
+                                                                 typename DType<DT>::T* __restrict__ y) {
+  using Tr = DType<DT>;
+  constexpr int NX = M + 2;
+  __shared__ float sd[NX * NX], sg[9], sm[MU * MU];
+  const int64_t s = blockIdx.x;
+  const int pt = threadIdx.x, i = pt / MU, j = pt % MU;
+  const bool live = pt < MU * MU;
+  auto rdadd = [&](float a, float b) { return acc32 ? __fadd_rn(a, b) : Tr::rd(__fadd_rn(a, b)); };
+  float stack[24];
+  float msum = 0.f;
+  for (int c = 0; c < C; ++c) {
+    __syncthreads();
+    const size_t base = ((size_t)c * S + s);
+    for (int e = threadIdx.x; e < NX * NX; e += blockDim.x) sd[e] = Tr::load(d + base * NX * NX + e);
+    for (int e = threadIdx.x; e < 9; e += blockDim.x) sg[e] = Tr::load(g + base * 9 + e);
+    __syncthreads();
+    if (!live) continue;
+    // U[i][j] = sum_b G[j][b] U1[i][b],  U1[i][b] = sum_a G[i][a] g[a][b]
+    float U1[3];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      float t = Tr::rd(__fmul_rn(Tr::rd(xp.G[i][0]), sg[0 * 3 + b]));
+#pragma unroll
+      for (int a = 1; a < 3; ++a) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.G[i][a]), sg[a * 3 + b]))));
+      U1[b] = t;
+    }
+    float u = Tr::rd(__fmul_rn(Tr::rd(xp.G[j][0]), U1[0]));
+#pragma unroll
+    for (int b = 1; b < 3; ++b) u = Tr::rd(__fadd_rn(u, Tr::rd(__fmul_rn(Tr::rd(xp.G[j][b]), U1[b]))));
+    // V[i][j] = sum_b BT[j][b] V1[i][b],  V1[i][b] = sum_a BT[i][a] d[a][b]
+    float v = 0.f;
+#pragma unroll
+    for (int b = 0; b < NX; ++b) {
+      float t = Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][0]), sd[0 * NX + b]));
+#pragma unroll
+      for (int a = 1; a < NX; ++a) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][a]), sd[a * NX + b]))));
+      const float term = Tr::rd(__fmul_rn(Tr::rd(xp.BT[j][b]), t));
+      v = b == 0 ? term : Tr::rd(__fadd_rn(v, term));
+    }
+    const float pc = Tr::rd(__fmul_rn(u, v));
+    if (csum == 0) {
+      msum = c == 0 ? pc : rdadd(msum, pc);
+    } else {
+      float val = pc;
+      int cnt = c, lvl = 0;
+      while (cnt & 1) val = rdadd(stack[lvl++], val), cnt >>= 1;
+      stack[lvl] = val;
+    }
+  }
+  if (live) {
+    if (csum == 1) {
+      // combine the stored partials from the lowest level up: sum = partial(high) + sum
+      bool first = true;
+      for (int lvl = 0; lvl < 24; ++lvl)
+        if ((C >> lvl) & 1) {
+          msum = first ? stack[lvl] : rdadd(stack[lvl], msum);
+          first = false;
+        }
+    }
+    sm[pt] = acc32 ? Tr::rd(msum) : msum;
+  }
+  __syncthreads();
+  if (pt < M * M) {
+    const int p = pt / M, q = pt % M;
+    // Y[p][q] = sum_jj AT[q][jj] Y1[p][jj],  Y1[p][jj] = sum_ii AT[p][ii] M[ii][jj]
+    float out = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < MU; ++jj) {
+      float t = Tr::rd(__fmul_rn(Tr::rd(xp.AT[p][0]), sm[0 * MU + jj]));
+#pragma unroll
+      for (int ii = 1; ii < MU; ++ii) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.AT[p][ii]), sm[ii * MU + jj]))));
+      const float term = Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][jj]), t));
+      out = jj == 0 ? term : Tr::rd(__fadd_rn(out, term));
+    }
+    y[s * M * M + pt] = Tr::cvt(out);
+  }
+}
+
+struct C2Args {
+  const void *d, *g;
+  int C;
+  int64_t S;
+  const XformParams* xp;
+  int csum, acc;
+  void* y;
+  cudaStream_t st;
+};
+template <int DT, int M, int MU>
+static void launch_c2(const C2Args& a) {
+  using TT = typename DType<DT>::T;
+  const int thr = (MU * MU + 31) / 32 * 32;
+  conv2d_tiles_paper_kernel<DT, M, MU><<<(unsigned)a.S, thr, 0, a.st>>>((const TT*)a.d, (const TT*)a.g, a.C, a.S,
+                                                                       *a.xp, a.csum, a.acc, (TT*)a.y);
+}
+using C2Fn = void (*)(const C2Args&);
+#define C2ROW(DT, M) {&launch_c2<DT, M, M + 2>, &launch_c2<DT, M, M + 3>, &launch_c2<DT, M, M + 4>}
+#define C2TAB(DT) {C2ROW(DT, 2), C2ROW(DT, 3), C2ROW(DT, 4), C2ROW(DT, 5), C2ROW(DT, 6), C2ROW(DT, 7), C2ROW(DT, 8)}
+static const C2Fn kC2[3][7][3] = {C2TAB(WINO_F32), C2TAB(WINO_F16), C2TAB(WINO_BF16)};
 
 // ------------------------------------------------------------------ K6: error statistics
 constexpr int kStatThreads = 256;
@@ -227,6 +380,23 @@ wino_status wino_conv1d_tiles(const void* x, const void* h, int64_t T, const win
   if (T == 0) return WINO_OK;
   C1Args a{x, h, T, &al->xp, y, reinterpret_cast<cudaStream_t>(stream)};
   kC1[per_op_rounding ? 1 : 0][dt][al->m - 2][dm](a);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+wino_status wino_conv2d_tiles_paper(const void* d, const void* g, int C, int64_t S, const wino_algo* al,
+                                   wino_dtype dt, int csum, int acc, void* y, void* stream) {
+  reset_launch_count();
+  if (!al || !d || !g || !y || C <= 0 || S < 0 || (csum != 0 && csum != 1) || (acc != 0 && acc != 1))
+    return set_last_error("bad argument"), WINO_E_ARG;
+  if (dt != WINO_F32 && dt != WINO_F16 && dt != WINO_BF16) return set_last_error("bad dtype"), WINO_E_ARG;
+  if (al->lowering != WINO_LOWER_SUBSOLVER) return set_last_error("2D paper tiles: SUBSOLVER algos only"), WINO_E_UNSUPPORTED;
+  const int dm = al->mu - al->m - 2;
+  if (dm < 0 || dm > 2 || al->m > 8) return set_last_error("2D paper tiles: m <= 8, mu in [m+2, m+4]"), WINO_E_UNSUPPORTED;
+  if (S > 0x7fffffff) return set_last_error("2D paper tiles: S < 2^31"), WINO_E_UNSUPPORTED;
+  if (S == 0) return WINO_OK;
+  C2Args a{d, g, C, S, &al->xp, csum, acc, y, reinterpret_cast<cudaStream_t>(stream)};
+  kC2[dt][al->m - 2][dm](a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
 }

@@ -787,9 +787,12 @@ __global__ void __launch_bounds__(128) input_transform_nhwc_direct(const typenam
                                                                    typename DType<DT>::T* __restrict__ V,
                                                                    size_t qstride, size_t plane) {
   using Tr = DType<DT>;
-  const int pi = blockIdx.x * blockDim.x + threadIdx.x;   // channel pair index
-  const int t = blockIdx.y;
-  if (2 * pi >= Cp) return;
+  // one thread per (tile, channel pair), pairs fastest: Cp / 2 is a multiple of 32,
+  // so a warp shares its tile; a flat 1D grid has no 65535-tile limit
+  const size_t id = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int P = Cp / 2;
+  if (id >= (size_t)T * P) return;
+  const int t = (int)(id / P), pi = (int)(id % P);
   const int ca = 2 * pi, cb = ca + 1;
   const int tj = t % tw, rest = t / tw, ti = rest % th, n = rest / th;
   if constexpr (k1_nchunk(NX, D) == 1) {
@@ -1022,7 +1025,8 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
 // KB output channels per CTA; TS = per-tile stride of the stage in elements
 // (+8: 16-byte aligned rows, and only 4-way bank conflicts for lane = tile)
 template <int M> struct K4N {
-  static constexpr int KB = M <= 4 ? 32 : 16;
+  // (16 channels x 144 pixels of fp32 for 32 tiles would need 296 KB of shared memory at m = 12)
+  static constexpr int KB = M <= 4 ? 32 : (M <= 10 ? 16 : 8);
   static constexpr int TS = M * M * KB + 8;
 };
 
@@ -1243,7 +1247,7 @@ static void launch_in_nhwc(const InArgs& a) {
     }
   }
   const int T = a.N * a.th * a.tw;
-  dim3 grid((a.Cp / 2 + 127) / 128, T);
+  dim3 grid((unsigned)(((size_t)T * (a.Cp / 2) + 127) / 128));
   pick_k1_nhwc_direct<DT, M, NX, D>(*a.xp)<<<grid, 128, 0, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th,
                                                                       a.tw, a.Cp, T, *a.xp, (TT*)a.V, a.qstride,
                                                                       a.plane);

@@ -493,10 +493,13 @@ np.save(sys.argv[1], np.concatenate(out))
 
 
 def test_fused_gemm_output_transform_matches_staged():
-    """The opt-in fused K3+K4 kernel (WINO_FUSED=1, output transform from L2) gives
-    bit-identical y to the staged K3 -> K4 pair (same fp32 arithmetic per
-    output; only where M lives differs).  Runs in a subprocess because the
-    switch is read once per process."""
+    """The fused K3+K4 kernel with split SMs (split.cu: tensor-core CTAs write M
+    to L2, CUDA-core CTAs transform and discard it) gives bit-identical y to the
+    staged K3 -> K4 pair (same fp32 arithmetic per output; only where M lives
+    differs) -- for ragged K (272: a partial 256-channel GEMM block and a partial
+    32-channel transform slice), ragged tiles, several tile blocks, and any SM
+    split or backpressure distance.  Subprocesses: the switches are read per
+    process (WINO_FUSED) or per call (WINO_SPLIT_*)."""
     import subprocess
     import sys
     code = r"""
@@ -505,10 +508,11 @@ sys.path.insert(0, '.')
 import datagen, paper_1905_05233_b200 as W
 from paper_1905_05233_b200.algos import canonical_spec
 out = []
-for name, dt in (('lin4', 'bf16'), ('sup1_6', 'fp16')):
+for name, dt, N, H, Wd in (('lin4', 'bf16', 3, 23, 19), ('sup1_6', 'fp16', 3, 23, 19), ('lin4', 'bf16', 8, 40, 37),
+                           ('sup1_6', 'bf16', 8, 41, 40), ('lin2', 'fp16', 4, 30, 30), ('lin8', 'bf16', 4, 33, 35)):
     spec, m = canonical_spec(name)
     a = W.WinoAlgo(spec, m)
-    x, w = datagen.layer(3, 96, 272, 23, 19, dt, seed=2)
+    x, w = datagen.layer(N, 96, 272, H, Wd, dt, seed=2)
     td = {'bf16': torch.bfloat16, 'fp16': torch.float16}[dt]
     y = W.wino_conv2d(torch.from_numpy(x).to(td).cuda(), torch.from_numpy(w).to(td).cuda(), a)
     torch.cuda.synchronize()
@@ -519,14 +523,18 @@ np.save(sys.argv[1], np.concatenate([o.ravel() for o in out]))
     import tempfile
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = []
-    for fused in ("0", "1"):
+    runs = [{"WINO_FUSED": "0"}, {"WINO_FUSED": "1"}, {"WINO_FUSED": "1", "WINO_SPLIT_LAG": "1", "WINO_SPLIT_R": "100"},
+            {"WINO_FUSED": "1", "WINO_SPLIT_R": "4", "WINO_SPLIT_LAG": "0"}]
+    for extra in runs:
         f = tempfile.NamedTemporaryFile(suffix=".npy", delete=False).name
-        env = dict(os.environ, WINO_FUSED=fused)
+        env = {k: v for k, v in os.environ.items() if not k.startswith("WINO_")}
+        env.update(extra)
         r = subprocess.run([sys.executable, "-c", code, f], cwd=root, env=env, capture_output=True, text=True,
                            timeout=300)
-        assert r.returncode == 0, r.stderr[-2000:]
+        assert r.returncode == 0, (extra, r.stderr[-2000:])
         res.append(np.load(f))
-    assert np.array_equal(res[0], res[1])
+    for i in range(1, len(res)):
+        assert np.array_equal(res[0], res[i]), runs[i]
 
 
 NHWC_CASES = [("lin4", "subsolver", 2, 64, 128, 28, 28, 1),     # TMA boxes, 64-channel blocks
@@ -534,7 +542,10 @@ NHWC_CASES = [("lin4", "subsolver", 2, 64, 128, 28, 28, 1),     # TMA boxes, 64-
               ("sup1_6", "subsolver", 1, 128, 136, 30, 30, 1),
               ("lin2", "subsolver", 1, 3, 64, 32, 32, 1),      # C = 3: direct-load fallback
               ("lin8", "subsolver", 1, 64, 64, 26, 26, 0),
-              ("sup1_4", "residue", 2, 72, 40, 19, 23, 1)]
+              ("sup1_4", "residue", 2, 72, 40, 19, 23, 1),
+              ("lin2", "subsolver", 6, 3, 8, 224, 224, 1),     # C = 3 direct-load kernel, T = 75264 > 65535 tiles
+              ("sup1_10", "subsolver", 1, 64, 64, 25, 27, 1),  # tiles beyond 8x8 (direct-load K1)
+              ("sup1_12", "subsolver", 1, 64, 64, 27, 29, 1)]
 
 
 @pytest.mark.parametrize("case", NHWC_CASES, ids=lambda c: f"{c[0]}-{c[1]}-C{c[3]}K{c[4]}-{c[5]}x{c[6]}p{c[7]}")
@@ -589,24 +600,79 @@ def test_host_io_chunked_equals_device_call(N, layout):
     assert torch.equal(yh, y_dev.cpu())
 
 
-def test_error_study_trends_on_gpu():
-    """Sec. 3.1 / Figure 1 (P:530-550) on the GPU path (scripts/error_study.py,
-    5000 paired random tiles, as P:531): fp32 error of the Toom-Cook sets grows with the
-    tile size in 1D and 2D, and at the 2D ratio 2.25 the a^2+1 set
-    W F(6x6) beats TC F(4x4) -- the same qualitative facts the
-    oracle's trend tests pin."""
+def _error_study():
     import importlib.util
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     spec = importlib.util.spec_from_file_location("error_study", os.path.join(root, "scripts", "error_study.py"))
     es = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(es)
+    return es
+
+
+def test_error_study_trends_on_gpu():
+    """Sec. 3.1 / Figure 1 (P:530-550) on the GPU path (scripts/error_study.py,
+    5000 random trials, each with its own kernel and tile, as P:531): fp32 error
+    of the Toom-Cook sets grows with the tile size in 1D and 2D, and at
+    the 2D ratio 2.25 the a^2+1 set W F(6x6) beats TC F(4x4) --
+    in the paper's per-op rounding and in the tensor-core layer."""
+    es = _error_study()
     rows = es.run(5000, dtypes=("fp32",), ns=(2, 4, 6, 8))
-    err = {(r["dim"], r["family"], r["n"]): r["mean_euclid"] for r in rows}
-    for dim in (1, 2):
-        lin = [err[(dim, "lin", n)] for n in (2, 4, 6, 8)]
-        assert all(a < b for a, b in zip(lin, lin[1:])), (dim, lin)
-    assert err[(2, "sup1[a^2+1]", 6)] < err[(2, "lin", 4)]
+    err = {(r["dim"], r["mode"], r["family"], r["n"]): r["mean_euclid"] for r in rows}
+    for dim, mode in ((1, "paper"), (2, "paper"), (2, "pipeline")):
+        lin = [err[(dim, mode, "lin", n)] for n in (2, 4, 6, 8)]
+        assert all(a < b for a, b in zip(lin, lin[1:])), (dim, mode, lin)
+    for mode in ("paper", "pipeline"):
+        assert err[(2, mode, "sup1[a^2+1]", 6)] < err[(2, mode, "lin", 4)], mode
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_error_study_matches_oracle(dtype):
+    """The GPU study's 2D numbers are the oracle's on the same trials: paper mode
+    bit for bit (K7 = oracle paper_conv2d_tiles), the pipeline-mode layer within
+    +-10 % of the oracle's pipeline emulation per point set (fresh kernel per
+    trial, P:531)."""
+    es = _error_study()
+    n, trials = 4, 640
+    d, g = es.trials2d(trials, n, 123)
+    dd, gd = datagen.to_dtype_values(d, dtype), datagen.to_dtype_values(g, dtype)
+    ref = es.direct2d(dd, gd)
+    td = TD[dtype]
+    for fam, spec in es.point_sets(n):
+        a = W.WinoAlgo(spec, n)
+        mods = T.parse_moduli(spec)
+        ts = T.make_transforms(mods, n)
+        yg = W.wino_conv2d_tiles_paper(torch.from_numpy(dd).to(td).cuda(), torch.from_numpy(gd).to(td).cuda(), a)
+        yo = P.paper_conv2d_tiles(ts, dd, gd, dtype)
+        assert es.errs(host(yg), ref) == es.errs(yo.astype(np.float64), ref), fam
+        yp = es.pipeline_diag(W, a, dd, gd, td)
+        yop = np.stack([P.pipeline_conv2d(ts, dd[:, s][None], gd[:, s][None], dtype, pad=0)[0, 0]
+                        for s in range(trials)])
+        eg, eo = es.errs(yp, ref)[0], es.errs(yop.astype(np.float64), ref)[0]
+        assert abs(eg / eo - 1) <= 0.10, (fam, eg, eo)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
+@pytest.mark.parametrize("name", ["lin4", "sup1_6", "lin8", "sup2_6", "lin2"])
+@pytest.mark.parametrize("C", [1, 5, 37])
+def test_conv2d_tiles_paper_bitwise(dtype, name, C):
+    """K7 (paper-mode multi-channel 2D tiles) equals the oracle's
+    paper_conv2d_tiles bit for bit in every channel-sum variant of P:611:
+    sequential / pairwise, dtype / fp32 accumulation."""
+    mods, m = T.canonical(name)
+    ts = T.make_transforms(mods, m)
+    a = W.WinoAlgo(T.moduli_spec(mods), m)
+    rng = np.random.default_rng(C)
+    S = 257
+    d = datagen.to_dtype_values(rng.normal(0, 1, (C, S, m + 2, m + 2)), dtype)
+    g = datagen.to_dtype_values(rng.normal(0, 1, (C, S, 3, 3)), dtype)
+    dd, gd = dev(d, dtype), dev(g, dtype)
+    for csum in ("sequential", "pairwise"):
+        for acc in ("dtype", "fp32"):
+            y = host(W.wino_conv2d_tiles_paper(dd, gd, a, csum, acc)).astype(np.float32)
+            yo = P.paper_conv2d_tiles(ts, d, g, dtype, csum=csum, acc=acc).astype(np.float32)
+            same = (y.view(np.uint32) == yo.view(np.uint32)) | (np.isnan(y) & np.isnan(yo))
+            assert same.all(), (csum, acc, int((~same).sum()))
 
 
 @pytest.mark.parametrize("name,dtype", [("lin8", "fp16"), ("lin8", "bf16"), ("lin6", "fp16"), ("sup1_8", "fp16")])

@@ -186,3 +186,33 @@ def test_pipeline_accumulates_M_in_fp32(dtype):
     w[0, :, 1, 1] = 1.0      # centre tap: y[i][j] = sum_c x[c][i+1][j+1]
     y = P.pipeline_conv2d(ts, x, w, dtype, pad=0)
     assert y[0, 0].tolist() == [[big + 2, 0.0], [0.0, 0.0]]
+
+
+# --------------------------------------------------------------------------- channel-sum boosters
+
+
+@pytest.mark.parametrize("case", _gold()["channel_sum"]["cases"], ids=lambda c: f'{c["dtype"]}-C{len(c["P"])}')
+@pytest.mark.parametrize("csum", ["sequential", "pairwise"])
+@pytest.mark.parametrize("acc", ["dtype", "fp32"])
+def test_paper_conv2d_tiles_channel_sum_variants(case, csum, acc):
+    """The channel sum of the paper-mode 2D tiles, sequential vs pairwise and
+    dtype vs fp32 (mixed precision) accumulation: channel c carries the product
+    P_c at the single Winograd point of the 1-point algorithm."""
+    dt = case["dtype"]
+    C = len(case["P"])
+    d = np.zeros((C, 1, 3, 3), np.float32)
+    d[:, 0, 0, 0] = case["P"]
+    g = np.zeros((C, 1, 3, 3), np.float32)
+    g[:, 0, 0, 0] = 1
+    got = P.paper_conv2d_tiles(_sum_algo(), d, g, dt, csum=csum, acc=acc)[0, 0, 0]
+    assert got == case[f"{csum}_{acc}"]
+
+
+def test_pairwise_sum_tree_shape():
+    """pairwise_sum's tree: h = the largest power of two below n (records the
+    association with strings)."""
+    add = lambda a, b: f"({a}+{b})"   # noqa: E731
+    assert P.pairwise_sum(list("abcde"), add) == "(((a+b)+(c+d))+e)"
+    assert P.pairwise_sum(list("abcdef"), add) == "(((a+b)+(c+d))+(e+f))"
+    assert P.pairwise_sum(list("abcdefg"), add) == "(((a+b)+(c+d))+((e+f)+g))"
+    assert P.pairwise_sum(list("a"), add) == "a"
