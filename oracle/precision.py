@@ -402,3 +402,47 @@ def _abs_bound_parts(ts, x, w, dtype, pad, C_acc, mma_rel):
     S_eta = _scatter_tiles(sep2(absAT, Me), N, K, th, tw, m, Ho, Wo)
     g = (8 + 2 * ts.n_x + 2 + C_acc + 2 * mu + 2) * u32 + mma_rel
     return S, g, u_d, S_eta
+
+
+def residue_elementwise_bound(rb, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05):
+    """First-order forward error bound of the residue-block pipeline
+    (pipeline_residue_conv2d; reading R1 applied to A3'):
+        |y - y_exact| <= (2 u_d + g) S + eta S_eta + u_d |y| + eta,
+    with S = |A_P|^T ( sum_units sum_c |W_unit| |V_in| ) |A_P| scattered to the
+    outputs, |W_unit| <= sum_terms |coef| (|G_P| |g| |G_P|^T)_term (the slab
+    combination before its single rounding), |V| <= |B_P|^T |d| |B_P|, and g the
+    fp32 error of the transforms, the slab combination (<= 4 terms) and the
+    channel x unit accumulation of each output point.  S_eta propagates the
+    absolute (underflow) errors of W and V."""
+    u_d = UNIT_ROUNDOFF[dtype]
+    u32 = UNIT_ROUNDOFF["fp32"]
+    m, D, nh = rb.n_o, rb.D, rb.n_h
+    nx = m + nh - 1
+    C = x.shape[1]
+    N, _, H, W = x.shape
+    K = w.shape[0]
+    absGP = np.abs(np.array([[float(v) for v in r] for r in rb.GP]))
+    absBPT = np.abs(np.array([[float(v) for v in r] for r in zip(*rb.BP)]))      # D x nx
+    absAPT = np.abs(np.array([[float(v) for v in r] for r in zip(*rb.AP)]))      # m x D
+    Ua = sep2(absGP, np.abs(np.asarray(w, np.float64)).transpose(2, 3, 0, 1))    # (D, D, K, C)
+    d, (Ho, Wo, th, tw) = halo_tiles(np.abs(np.asarray(x, np.float64)), m, nx, pad)
+    Va = sep2(absBPT, d).transpose(0, 1, 2, 4, 5, 3).reshape(D * D, -1, C)        # (D^2, T, C)
+    Tn = Va.shape[1]
+    Z = np.zeros((D * D, K, Tn))
+    Ze = np.zeros((D * D, K, Tn))
+    per_point = np.zeros(D * D, int)
+    eta = ETA[dtype]
+    for (po, pi, (sI, nI, phI), (sJ, nJ, phJ), (k, l, kk, ll)) in residue_slabs(rb):
+        Wa = np.zeros((K, C))
+        for a in range(nI):
+            for b in range(nJ):
+                coef = abs(float(phI[a][kk][k] * phJ[b][ll][l]))
+                if coef:
+                    Wa += coef * Ua[sI + a, sJ + b]
+        Z[po] += Wa @ Va[pi].T
+        Ze[po] += Wa.sum(axis=1)[:, None] + Va[pi].sum(axis=1)[None, :] + eta * C
+        per_point[po] += 1
+    S = _scatter_tiles(sep2(absAPT, Z.reshape(D, D, K, Tn)), N, K, th, tw, m, Ho, Wo)
+    S_eta = _scatter_tiles(sep2(absAPT, Ze.reshape(D, D, K, Tn)), N, K, th, tw, m, Ho, Wo)
+    g = (8 + 2 * nx + 2 + 4 + C * int(per_point.max()) + 2 * D + 2) * u32 + mma_rel
+    return safety * ((2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta)

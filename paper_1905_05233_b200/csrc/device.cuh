@@ -20,18 +20,22 @@ template <> struct DType<WINO_F32> {
   static __device__ __forceinline__ float load(const T* p) { return *p; }
   static __device__ __forceinline__ T cvt(float v) { return v; }
   static __device__ __forceinline__ float rd(float v) { return v; }
+  static __device__ __forceinline__ float2 rd2(float2 v) { return v; }
 };
 template <> struct DType<WINO_F16> {
   using T = __half;
   static __device__ __forceinline__ float load(const T* p) { return __half2float(*p); }
   static __device__ __forceinline__ T cvt(float v) { return __float2half_rn(v); }
   static __device__ __forceinline__ float rd(float v) { return __half2float(__float2half_rn(v)); }
+  // two values per conversion (cvt.rn.f16x2.f32): the same RNE rounding per element
+  static __device__ __forceinline__ float2 rd2(float2 v) { return __half22float2(__float22half2_rn(v)); }
 };
 template <> struct DType<WINO_BF16> {
   using T = __nv_bfloat16;
   static __device__ __forceinline__ float load(const T* p) { return __bfloat162float(*p); }
   static __device__ __forceinline__ T cvt(float v) { return __float2bfloat16_rn(v); }
   static __device__ __forceinline__ float rd(float v) { return __bfloat162float(__float2bfloat16_rn(v)); }
+  static __device__ __forceinline__ float2 rd2(float2 v) { return __bfloat1622float2(__float22bfloat162_rn(v)); }
 };
 
 inline size_t dtype_size(wino_dtype dt) { return dt == WINO_F32 ? 4 : 2; }

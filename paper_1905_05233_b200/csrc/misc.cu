@@ -1,6 +1,8 @@
 // misc.cu -- K5 batched 1D tiles (BASELINE cfg 2), K6 error statistics, the
 // fp64 direct-convolution reference of the metric path, launch accounting.
+#include <cstring>
 #include <string>
+#include <type_traits>
 
 #include "device.cuh"
 #include "geometry.hpp"
@@ -52,54 +54,145 @@ int num_sms() {
 // scalar multiply/add in fp32 without contraction (__fmul_rn / __fadd_rn), cast
 // to the dtype after each op, ascending index from the first product, matrix
 // entries cast once.  PAPER=false: fp32 internally, u, v, y rounded.
+// A thread owns two adjacent tiles: their x / h / y runs are contiguous, so they
+// move with 4- or 8-byte vector accesses, and every operation is a packed fp32x2
+// one (FMUL2 / FADD2 / FFMA2, two-element conversions) -- per element the same
+// IEEE operations in the same order, so results are unchanged bit for bit.
+template <typename TT>
+__device__ __forceinline__ void load_run2(const TT* __restrict__ p, int n2, float* out, bool vec) {
+  // out[0 .. 2 * n2) = p[0 .. 2 * n2) as fp32; vec: p is 4-byte (16-bit) / 8-byte (fp32) aligned
+  if (vec) {
+    if constexpr (sizeof(TT) == 2) {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k >= n2) break;
+        const uint32_t wv = __ldg(q + k);
+        TT lo, hi;
+        const uint16_t l16 = (uint16_t)(wv & 0xFFFFu), h16 = (uint16_t)(wv >> 16);
+        memcpy(&lo, &l16, 2);
+        memcpy(&hi, &h16, 2);
+        out[2 * k] = DType<std::is_same<TT, __half>::value ? WINO_F16 : WINO_BF16>::load(&lo);
+        out[2 * k + 1] = DType<std::is_same<TT, __half>::value ? WINO_F16 : WINO_BF16>::load(&hi);
+      }
+    } else {
+      const float2* q = reinterpret_cast<const float2*>(p);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k >= n2) break;
+        const float2 v = __ldg(q + k);
+        out[2 * k] = v.x, out[2 * k + 1] = v.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k >= 2 * n2) break;
+      if constexpr (sizeof(TT) == 4) out[k] = p[k];
+      else out[k] = DType<std::is_same<TT, __half>::value ? WINO_F16 : WINO_BF16>::load(p + k);
+    }
+  }
+}
+
 template <int DT, int M, int MU, bool PAPER>
 __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<DT>::T* __restrict__ x,
                                                            const typename DType<DT>::T* __restrict__ h, int64_t T,
                                                            const __grid_constant__ XformParams xp,
-                                                           typename DType<DT>::T* __restrict__ y) {
+                                                           typename DType<DT>::T* __restrict__ y, int vec) {
   using Tr = DType<DT>;
+  using TT = typename Tr::T;
   constexpr int NX = M + 2;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (t >= T) return;
-  float hv[3], xv[NX];
+  const bool two = t + 1 < T;
+  float xr[2 * NX], hr[6];
+  if (two) {
+    load_run2<TT>(x + t * NX, NX, xr, vec != 0);
+    load_run2<TT>(h + t * 3, 3, hr, vec != 0);
+  } else {
 #pragma unroll
-  for (int j = 0; j < 3; ++j) hv[j] = Tr::load(h + t * 3 + j);
+    for (int j = 0; j < NX; ++j) xr[j] = Tr::load(x + t * NX + j), xr[NX + j] = 0.f;
 #pragma unroll
-  for (int j = 0; j < NX; ++j) xv[j] = Tr::load(x + t * NX + j);
-  float p[MU];
+    for (int j = 0; j < 3; ++j) hr[j] = Tr::load(h + t * 3 + j), hr[3 + j] = 0.f;
+  }
+  float2 hv[3], xv[NX];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) hv[j] = make_float2(hr[j], hr[3 + j]);
+#pragma unroll
+  for (int j = 0; j < NX; ++j) xv[j] = make_float2(xr[j], xr[NX + j]);
+  auto bc = [](float c) { return make_float2(c, c); };
+  // paper-mode products and sums: packed FMUL2 / FADD2 in 16-bit (a rounding sits
+  // between every pair); in fp32 nothing separates them, and the packed pair may
+  // be contracted into FFMA2, so fp32 keeps the scalar non-contracting intrinsics
+  auto mul = [](float2 a, float2 b) {
+    if constexpr (DT == WINO_F32) return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+    else return __fmul2_rn(a, b);
+  };
+  auto add = [](float2 a, float2 b) {
+    if constexpr (DT == WINO_F32) return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+    else return __fadd2_rn(a, b);
+  };
+  float2 p[MU];
 #pragma unroll
   for (int i = 0; i < MU; ++i) {
-    float u, v;
+    float2 u, v;
     if constexpr (PAPER) {
-      u = Tr::rd(__fmul_rn(Tr::rd(xp.G[i][0]), hv[0]));
+      u = Tr::rd2(mul(bc(Tr::rd(xp.G[i][0])), hv[0]));
 #pragma unroll
-      for (int j = 1; j < 3; ++j) u = Tr::rd(__fadd_rn(u, Tr::rd(__fmul_rn(Tr::rd(xp.G[i][j]), hv[j]))));
-      v = Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][0]), xv[0]));
+      for (int j = 1; j < 3; ++j) u = Tr::rd2(add(u, Tr::rd2(mul(bc(Tr::rd(xp.G[i][j])), hv[j]))));
+      v = Tr::rd2(mul(bc(Tr::rd(xp.BT[i][0])), xv[0]));
 #pragma unroll
-      for (int j = 1; j < NX; ++j) v = Tr::rd(__fadd_rn(v, Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][j]), xv[j]))));
-      p[i] = Tr::rd(__fmul_rn(u, v));
+      for (int j = 1; j < NX; ++j) v = Tr::rd2(add(v, Tr::rd2(mul(bc(Tr::rd(xp.BT[i][j])), xv[j]))));
+      p[i] = Tr::rd2(mul(u, v));
     } else {
-      u = 0.f, v = 0.f;
+      u = make_float2(0.f, 0.f), v = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int j = 0; j < 3; ++j) u = fmaf(xp.G[i][j], hv[j], u);
+      for (int j = 0; j < 3; ++j) u = __ffma2_rn(bc(xp.G[i][j]), hv[j], u);
 #pragma unroll
-      for (int j = 0; j < NX; ++j) v = fmaf(xp.BT[i][j], xv[j], v);
-      p[i] = __fmul_rn(Tr::rd(u), Tr::rd(v));
+      for (int j = 0; j < NX; ++j) v = __ffma2_rn(bc(xp.BT[i][j]), xv[j], v);
+      p[i] = __fmul2_rn(Tr::rd2(u), Tr::rd2(v));
     }
   }
+  float yo[2][M];
 #pragma unroll
   for (int q = 0; q < M; ++q) {
-    float acc;
+    float2 acc;
     if constexpr (PAPER) {
-      acc = Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][0]), p[0]));
+      acc = Tr::rd2(mul(bc(Tr::rd(xp.AT[q][0])), p[0]));
 #pragma unroll
-      for (int i = 1; i < MU; ++i) acc = Tr::rd(__fadd_rn(acc, Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][i]), p[i]))));
+      for (int i = 1; i < MU; ++i) acc = Tr::rd2(add(acc, Tr::rd2(mul(bc(Tr::rd(xp.AT[q][i])), p[i]))));
     } else {
-      acc = 0.f;
+      acc = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < MU; ++i) acc = fmaf(xp.AT[q][i], p[i], acc);
+      for (int i = 0; i < MU; ++i) acc = __ffma2_rn(bc(xp.AT[q][i]), p[i], acc);
     }
-    y[t * M + q] = Tr::cvt(acc);
+    yo[0][q] = acc.x, yo[1][q] = acc.y;
+  }
+  if (two && vec) {
+    if constexpr (sizeof(TT) == 2) {
+      uint32_t* q = reinterpret_cast<uint32_t*>(y + t * M);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const float a0 = yo[(2 * k) / M][(2 * k) % M];
+        const float a1 = yo[(2 * k + 1) / M][(2 * k + 1) % M];
+        TT e0 = Tr::cvt(a0), e1 = Tr::cvt(a1);
+        uint16_t b0, b1;
+        memcpy(&b0, &e0, 2);
+        memcpy(&b1, &e1, 2);
+        q[k] = (uint32_t)b0 | ((uint32_t)b1 << 16);
+      }
+    } else {
+      float2* q = reinterpret_cast<float2*>(y + t * M);
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        q[k] = make_float2(yo[(2 * k) / M][(2 * k) % M], yo[(2 * k + 1) / M][(2 * k + 1) % M]);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < M; ++q) y[t * M + q] = Tr::cvt(yo[0][q]);
+    if (two)
+#pragma unroll
+      for (int q = 0; q < M; ++q) y[(t + 1) * M + q] = Tr::cvt(yo[1][q]);
   }
 }
 
@@ -113,8 +206,14 @@ struct C1Args {
 template <int DT, int M, int MU, bool P>
 static void launch_c1(const C1Args& a) {
   using Tr = DType<DT>;
-  conv1d_tiles_kernel<DT, M, MU, P><<<(unsigned)((a.T + 127) / 128), 128, 0, a.st>>>(
-      (const typename Tr::T*)a.x, (const typename Tr::T*)a.h, a.T, *a.xp, (typename Tr::T*)a.y);
+  // vector accesses when x, h and y are aligned for them (each thread's runs start
+  // at multiples of 2 tiles: 4-byte aligned in 16-bit, 8-byte in fp32)
+  const uintptr_t al = sizeof(typename Tr::T) == 2 ? 4 : 8;
+  const int vec = (reinterpret_cast<uintptr_t>(a.x) % al == 0 && reinterpret_cast<uintptr_t>(a.h) % al == 0 &&
+                   reinterpret_cast<uintptr_t>(a.y) % al == 0) ? 1 : 0;
+  const int64_t thr = (a.T + 1) / 2;
+  conv1d_tiles_kernel<DT, M, MU, P><<<(unsigned)((thr + 127) / 128), 128, 0, a.st>>>(
+      (const typename Tr::T*)a.x, (const typename Tr::T*)a.h, a.T, *a.xp, (typename Tr::T*)a.y, vec);
 }
 using C1Fn = void (*)(const C1Args&);
 #define C1ROW(DT, M, P) {&launch_c1<DT, M, M + 2, P>, &launch_c1<DT, M, M + 3, P>, &launch_c1<DT, M, M + 4, P>}

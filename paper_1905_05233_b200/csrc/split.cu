@@ -50,7 +50,7 @@ struct SplitArgs {
   int* fixed;          // [nMB] channels transformed
   int dbg;             // timing experiments only (WINO_SPLIT_DBG): 1 no L2 discard, 2 no transform math,
                        // 4 transform CTAs exit at once (GEMM alone; no backpressure), 8 no publication,
-                       // 16 p-major GEMM item order (with 4 only)
+                       // 16 p-major GEMM item order (with 4 only), 32 no L2 cache-policy hints
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -80,6 +80,40 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                    smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// L2 eviction-priority policies (createpolicy): the streamed V tiles, the
+// consumed M pieces and y go first, the M written for the transform role stays.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d_hint(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                  int c3, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 // wait until at most n of this thread's bulk store groups are pending (n <= 8)
 __device__ __forceinline__ void bulk_wait_pending(int n) {
   switch (n) {
@@ -179,6 +213,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
     const int per_mb = Q * sa.nNB;
     const int nItems = sa.nMB * per_mb;
     const int KB = Cp / Cfg::BK;
@@ -212,7 +247,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
               mbar_wait(&empty[stage], phase ^ 1);
               mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
               uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-              tma_load_3d(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi);
+              if (sa.dbg & 32) tma_load_3d(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi);
+              else tma_load_3d_hint(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi, pol_first);
               tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
               if (++stage == STAGES) stage = 0, phase ^= 1;
             }
@@ -282,7 +318,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
           fence_proxy_async_shared();
           named_bar_sync(1, 128);
           if (storer) {
-            tma_store_4d(&tmMb, buf, 0, p, nb * BN + j0, mb);
+            if (sa.dbg & 32) tma_store_4d(&tmMb, buf, 0, p, nb * BN + j0, mb);
+            else tma_store_4d_hint(&tmMb, buf, 0, p, nb * BN + j0, mb, pol_last);
             bulk_commit();
           }
           ++chunk, ++nbox;
@@ -339,6 +376,7 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
   __syncthreads();
   const int nItems = sa.nMB * sa.nKS;
   const int need = Q * sa.nNB;
+  const uint64_t pol_first = policy_evict_first();
   if (warp == 8) {
     if (lane == 0) {
       int s = 0;
@@ -352,7 +390,8 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
           const int kc = min(KP, nk - j);
           const uint32_t bytes = (uint32_t)(kc * piece * 4);
           mbar_arrive_expect_tx(&full[b], bytes);
-          bulk_load(ring + (size_t)b * slotf, sa.Mb + ((size_t)mb * K + k0 + j) * piece, bytes, &full[b]);
+          bulk_load_hint(ring + (size_t)b * slotf, sa.Mb + ((size_t)mb * K + k0 + j) * piece, bytes, &full[b],
+                         pol_first);
         }
       }
     }

@@ -139,7 +139,15 @@ def test_domain_gemm_isolated(dtype, name, lowering, T_, C, K):
     M = W.wino_domain_gemm(W.v_from_dense(dev(Vh, dtype)), dev(Uh, dtype), a, C, K, T_)
     torch.cuda.synchronize()
     got = host(M)[:, :, :T_]
-    out_pt, in_pt, *_ = a.unit_table()
+    # the unit -> (output point, input point) pairs come from the oracle (O6), and
+    # the library's schedule must list the same units in the same order
+    if lowering == "subsolver":
+        pairs = [(q, q) for q in range(Q)]
+    else:
+        pairs = [(po, pi) for (po, pi, *_r) in P.residue_slabs(ref)]
+    out_pt, in_pt = [p[0] for p in pairs], [p[1] for p in pairs]
+    lib_out, lib_in, *_ = a.unit_table()
+    assert list(lib_out) == out_pt and list(lib_in) == in_pt
     want = np.zeros((Q, K, T_))
     aw = np.zeros((Q, K, T_))
     for u in range(S):
@@ -217,6 +225,10 @@ def _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad, xdist="relu_normal"
         assert not bad.any(), (int(bad.sum()), float(np.abs(yg - yref).max()))
     else:
         yo = P.pipeline_residue_conv2d(ref, x, w, dtype, pad)
+        bound = P.residue_elementwise_bound(ref, x, w, dtype, yref, pad,
+                                            mma_rel=2.0 ** -20 if dtype == "fp32" else 0.0)
+        bad = np.abs(yg - yref) > bound
+        assert not bad.any(), (int(bad.sum()), float(np.abs(yg - yref).max()))
     sg = MT.summary(MT.stats8(yg, yref, m))
     so = MT.summary(MT.stats8(yo, yref, m))
     return sg, so, m
@@ -252,7 +264,8 @@ def test_layer(case, dtype):
     sg, so, m = _layer_check(name, lowering, dtype, N, C, K, H, Wd, pad)
     if dtype == "fp32":
         assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3), sg
-    elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
+    elif so["nonfinite"] == 0:
+        # including the fp16 range-collapse cases (lin8: mean relative error >> 1)
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
     assert sg["nonfinite"] == so["nonfinite"]
 
@@ -285,6 +298,24 @@ def test_ranking_linear_vs_superlinear(dtype):
         errs_g[name], errs_o[name] = sg["mean_rel"], so["mean_rel"]
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10
     assert (errs_g["sup1_6"] < errs_g["lin4"]) == (errs_o["sup1_6"] < errs_o["lin4"]) == True  # noqa: E712
+
+
+def test_ranking_cfg3_full_size():
+    """BASELINE cfg3 at full size (N=32, C=K=256, 56x56, fp16): the equal-ratio
+    pair of P:596 -- W F(6x6)+a^2+1 more accurate than TC F(4x4) -- on the GPU
+    as in the oracle's emulation of the same whole layer, each within +-10 %."""
+    c = dict(datagen.CONFIGS["cfg3"])
+    x, w = datagen.layer(c["N"], c["C"], c["K"], c["H"], c["W"], "fp16", seed=0, xdist=c["xdist"])
+    xd, wd = dev(x, "fp16"), dev(w, "fp16")
+    yr = W.wino_direct_conv2d_f64(xd, wd, 1)
+    yref = host(yr)
+    eg, eo = {}, {}
+    for name in ("lin4", "sup1_6"):
+        a, ref, m = algo_pair(name)
+        eg[name] = W.summary(W.wino_error_stats(W.wino_conv2d(xd, wd, a), yr, m))["mean_rel"]
+        eo[name] = MT.summary(MT.stats8(P.pipeline_conv2d(ref, x, w, "fp16"), yref, m))["mean_rel"]
+        assert abs(eg[name] / eo[name] - 1) <= 0.10, (name, eg[name], eo[name])
+    assert eg["sup1_6"] < eg["lin4"] and eo["sup1_6"] < eo["lin4"]
 
 
 def test_edge_cases():
@@ -385,7 +416,9 @@ def test_direct_f64_kernel(dtype):
 
 @pytest.mark.parametrize("cfg,name,dtype", [("cfg3", "lin4", "fp16"), ("cfg3", "sup1_6", "fp16"),
                                             ("cfg5", "lin4", "bf16"), ("cfg5", "sup1_6", "bf16"),
-                                            ("cfg5", "lin4", "fp32")])
+                                            ("cfg5", "lin4", "fp32")] +
+                         [("cfg5", n, d) for n in ("lin5", "lin7", "sup1_3", "sup1_5", "sup1_7")
+                          for d in ("fp32", "fp16", "bf16")])
 def test_full_size_sampled(cfg, name, dtype):
     """Full BASELINE size in the launch configuration bench.py times; the oracle
     recomputes a sample of images (images are independent)."""
@@ -408,7 +441,7 @@ def test_full_size_sampled(cfg, name, dtype):
     so = MT.summary(MT.stats8(yo, yref, m))
     ss = MT.summary(MT.stats8(yg, yref, m))
     if dtype == "fp32":
-        assert sg["rel_l1"] <= 1e-4
+        assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3)
     else:
         assert abs(ss["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (ss, so)
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.15, (sg, so)   # whole layer vs sample
@@ -573,7 +606,7 @@ def test_layer_nhwc(case, dtype):
     so = MT.summary(MT.stats8(yo, yref, m))
     if dtype == "fp32":
         assert sg["rel_l1"] <= (1e-4 if m <= 4 else 1e-3), sg
-    elif so["nonfinite"] == 0 and so["mean_rel"] < 1:
+    elif so["nonfinite"] == 0:
         assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
 
 

@@ -292,3 +292,20 @@ def test_pow2_scaling_fixes_fp16_range_collapse():
         res[dt] = (e0, e1)
     assert res["fp16"][0] > 1.0 and res["fp16"][1] < 0.5, res
     assert abs(res["bf16"][1] / res["bf16"][0] - 1) < 0.02, res
+
+
+@pytest.mark.parametrize("name,dtype", [("sup1_4", "fp16"), ("sup1_6", "bf16"), ("sup2_4", "fp16"), ("sup1_4", "fp32")])
+def test_residue_pipeline_within_its_forward_bound(name, dtype):
+    """The residue-block pipeline (A3') stays inside its own a-priori forward error
+    bound (first order, worst case over signs), and a wrong result -- the layer
+    with a 1 % (fp32) / 50 % (16-bit) weight error -- leaves it somewhere."""
+    x, w = datagen.layer(2, 24, 8, 13, 11, dtype, seed=4)
+    yref = CV.direct_conv2d_f64(x, w, 1)
+    mods, m = T.canonical(name)
+    rb = T.residue_blocks(mods, m)
+    y = P.pipeline_residue_conv2d(rb, x, w, dtype)
+    bound = P.residue_elementwise_bound(rb, x, w, dtype, yref)
+    assert (np.abs(y - yref) <= bound).all()
+    ts = T.make_transforms(mods, m)
+    bad = P.pipeline_conv2d(ts, x, w * (1.01 if dtype == "fp32" else 1.5), dtype)
+    assert (np.abs(bad - yref) > bound).any()
