@@ -51,7 +51,7 @@ _SIGS = {
     "wino_domain_gemm": (_I, [_P, _P, _I, _I, _I, _P, _I, _P, _P]),
     "wino_output_transform": (_I, [_P, _I, _I, _I, _I, _I, _P, _I, _I, _P, _P]),
     "wino_conv1d_tiles": (_I, [_P, _P, ctypes.c_int64, _P, _I, _I, _P, _P]),
-    "wino_conv2d_tiles_paper": (_I, [_P, _P, _I, ctypes.c_int64, _P, _I, _I, _I, _P, _P]),
+    "wino_conv2d_tiles_paper": (_I, [_P, _P, _I, ctypes.c_int64, _P, _I, _I, _I, _I, _P, _P]),
     "wino_error_stats_scratch": (ctypes.c_size_t, [_I, _I, _I, _I, _I]),
     "wino_error_stats": (_I, [_P, _I, _P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "wino_direct_conv2d_f64": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _P, _P]),

@@ -290,17 +290,18 @@ def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None,
 # --------------------------------------------------------------------------- 1D tiles / metrics
 
 
-def wino_conv1d_tiles(x, h, algo, per_op_rounding=True, stream=None):
+def wino_conv1d_tiles(x, h, algo, per_op_rounding=True, stream=None, bf16_mode="rne"):
     T = x.shape[0]
     assert x.shape == (T, algo.m + 2) and h.shape == (T, 3) and x.dtype == h.dtype
     y = torch.empty((T, algo.m), dtype=x.dtype, device=x.device)
     with torch.cuda.device(x.device):
         check(lib().wino_conv1d_tiles(_ptr(x.contiguous()), _ptr(h.contiguous()), T, algo.handle, _dt(x),
-                                      1 if per_op_rounding else 0, _ptr(y), _stream(stream, x.device)))
+                                      (1 if per_op_rounding else 0) | (2 if bf16_mode == "trunc" else 0), _ptr(y),
+                                      _stream(stream, x.device)))
     return y
 
 
-def wino_conv2d_tiles_paper(d, g, algo, csum="sequential", acc="dtype", stream=None):
+def wino_conv2d_tiles_paper(d, g, algo, csum="sequential", acc="dtype", bf16_mode="rne", stream=None):
     """Paper-mode multi-channel 2D tiles: d [C][S][m+2][m+2], g [C][S][3][3] ->
     Y [S][m][m] (include/wino.h wino_conv2d_tiles_paper)."""
     C, S = d.shape[:2]
@@ -311,7 +312,7 @@ def wino_conv2d_tiles_paper(d, g, algo, csum="sequential", acc="dtype", stream=N
     with torch.cuda.device(d.device):
         check(lib().wino_conv2d_tiles_paper(_ptr(d.contiguous()), _ptr(g.contiguous()), C, S, algo.handle, _dt(d),
                                             {"sequential": 0, "pairwise": 1}[csum], {"dtype": 0, "fp32": 1}[acc],
-                                            _ptr(y), _stream(stream, d.device)))
+                                            {"rne": 0, "trunc": 1}[bf16_mode], _ptr(y), _stream(stream, d.device)))
     return y
 
 

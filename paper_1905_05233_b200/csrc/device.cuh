@@ -38,6 +38,38 @@ template <> struct DType<WINO_BF16> {
   static __device__ __forceinline__ float2 rd2(float2 v) { return __bfloat1622float2(__float22bfloat162_rn(v)); }
 };
 
+// bf16 by truncation (reading A10's switch: drop the low 16 bits of the fp32
+// pattern; NaNs stay quiet NaNs), for the paper-mode tile kernels.
+__device__ __forceinline__ float bf16_trunc(float v) {
+  const uint32_t b = __float_as_uint(v);
+  return __uint_as_float((v != v) ? ((b & 0xFFFF0000u) | 0x00400000u) : (b & 0xFFFF0000u));
+}
+// rounding of the storage dtype with a runtime mode: trunc applies to bf16 only
+template <int DT>
+struct RdMode {
+  using Tr = DType<DT>;
+  using T = typename Tr::T;
+  bool trunc;
+  __device__ __forceinline__ float rd(float v) const {
+    if constexpr (DT == WINO_BF16) {
+      if (trunc) return bf16_trunc(v);
+    }
+    return Tr::rd(v);
+  }
+  __device__ __forceinline__ float2 rd2(float2 v) const {
+    if constexpr (DT == WINO_BF16) {
+      if (trunc) return make_float2(bf16_trunc(v.x), bf16_trunc(v.y));
+    }
+    return Tr::rd2(v);
+  }
+  __device__ __forceinline__ T cvt(float v) const {
+    if constexpr (DT == WINO_BF16) {
+      if (trunc) return __ushort_as_bfloat16((unsigned short)(__float_as_uint(bf16_trunc(v)) >> 16));
+    }
+    return Tr::cvt(v);
+  }
+};
+
 inline size_t dtype_size(wino_dtype dt) { return dt == WINO_F32 ? 4 : 2; }
 
 // Store one output-tile row v[0..M) (rounded to the storage dtype) at row[0..valid)

@@ -94,7 +94,7 @@ __device__ __forceinline__ void load_run2(const TT* __restrict__ p, int n2, floa
   }
 }
 
-template <int DT, int M, int MU, bool PAPER>
+template <int DT, int M, int MU, bool PAPER, bool TRUNC>
 __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<DT>::T* __restrict__ x,
                                                            const typename DType<DT>::T* __restrict__ h, int64_t T,
                                                            const __grid_constant__ XformParams xp,
@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<
   using Tr = DType<DT>;
   using TT = typename Tr::T;
   constexpr int NX = M + 2;
+  const RdMode<DT> R{TRUNC};   // compile-time mode: no per-op branch
   const int64_t t = 2 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (t >= T) return;
   const bool two = t + 1 < T;
@@ -137,20 +138,20 @@ __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<
   for (int i = 0; i < MU; ++i) {
     float2 u, v;
     if constexpr (PAPER) {
-      u = Tr::rd2(mul(bc(Tr::rd(xp.G[i][0])), hv[0]));
+      u = R.rd2(mul(bc(R.rd(xp.G[i][0])), hv[0]));
 #pragma unroll
-      for (int j = 1; j < 3; ++j) u = Tr::rd2(add(u, Tr::rd2(mul(bc(Tr::rd(xp.G[i][j])), hv[j]))));
-      v = Tr::rd2(mul(bc(Tr::rd(xp.BT[i][0])), xv[0]));
+      for (int j = 1; j < 3; ++j) u = R.rd2(add(u, R.rd2(mul(bc(R.rd(xp.G[i][j])), hv[j]))));
+      v = R.rd2(mul(bc(R.rd(xp.BT[i][0])), xv[0]));
 #pragma unroll
-      for (int j = 1; j < NX; ++j) v = Tr::rd2(add(v, Tr::rd2(mul(bc(Tr::rd(xp.BT[i][j])), xv[j]))));
-      p[i] = Tr::rd2(mul(u, v));
+      for (int j = 1; j < NX; ++j) v = R.rd2(add(v, R.rd2(mul(bc(R.rd(xp.BT[i][j])), xv[j]))));
+      p[i] = R.rd2(mul(u, v));
     } else {
       u = make_float2(0.f, 0.f), v = make_float2(0.f, 0.f);
 #pragma unroll
       for (int j = 0; j < 3; ++j) u = __ffma2_rn(bc(xp.G[i][j]), hv[j], u);
 #pragma unroll
       for (int j = 0; j < NX; ++j) v = __ffma2_rn(bc(xp.BT[i][j]), xv[j], v);
-      p[i] = __fmul2_rn(Tr::rd2(u), Tr::rd2(v));
+      p[i] = __fmul2_rn(R.rd2(u), R.rd2(v));
     }
   }
   float yo[2][M];
@@ -158,9 +159,9 @@ __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<
   for (int q = 0; q < M; ++q) {
     float2 acc;
     if constexpr (PAPER) {
-      acc = Tr::rd2(mul(bc(Tr::rd(xp.AT[q][0])), p[0]));
+      acc = R.rd2(mul(bc(R.rd(xp.AT[q][0])), p[0]));
 #pragma unroll
-      for (int i = 1; i < MU; ++i) acc = Tr::rd2(add(acc, Tr::rd2(mul(bc(Tr::rd(xp.AT[q][i])), p[i]))));
+      for (int i = 1; i < MU; ++i) acc = R.rd2(add(acc, R.rd2(mul(bc(R.rd(xp.AT[q][i])), p[i]))));
     } else {
       acc = make_float2(0.f, 0.f);
 #pragma unroll
@@ -175,7 +176,7 @@ __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<
       for (int k = 0; k < M; ++k) {
         const float a0 = yo[(2 * k) / M][(2 * k) % M];
         const float a1 = yo[(2 * k + 1) / M][(2 * k + 1) % M];
-        TT e0 = Tr::cvt(a0), e1 = Tr::cvt(a1);
+        TT e0 = R.cvt(a0), e1 = R.cvt(a1);
         uint16_t b0, b1;
         memcpy(&b0, &e0, 2);
         memcpy(&b1, &e1, 2);
@@ -189,10 +190,10 @@ __global__ void __launch_bounds__(128) conv1d_tiles_kernel(const typename DType<
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < M; ++q) y[t * M + q] = Tr::cvt(yo[0][q]);
+    for (int q = 0; q < M; ++q) y[t * M + q] = R.cvt(yo[0][q]);
     if (two)
 #pragma unroll
-      for (int q = 0; q < M; ++q) y[(t + 1) * M + q] = Tr::cvt(yo[1][q]);
+      for (int q = 0; q < M; ++q) y[(t + 1) * M + q] = R.cvt(yo[1][q]);
   }
 }
 
@@ -202,6 +203,7 @@ struct C1Args {
   const XformParams* xp;
   void* y;
   cudaStream_t st;
+  int trunc;
 };
 template <int DT, int M, int MU, bool P>
 static void launch_c1(const C1Args& a) {
@@ -212,7 +214,15 @@ static void launch_c1(const C1Args& a) {
   const int vec = (reinterpret_cast<uintptr_t>(a.x) % al == 0 && reinterpret_cast<uintptr_t>(a.h) % al == 0 &&
                    reinterpret_cast<uintptr_t>(a.y) % al == 0) ? 1 : 0;
   const int64_t thr = (a.T + 1) / 2;
-  conv1d_tiles_kernel<DT, M, MU, P><<<(unsigned)((thr + 127) / 128), 128, 0, a.st>>>(
+  const dim3 grid((unsigned)((thr + 127) / 128));
+  if constexpr (DT == WINO_BF16) {
+    if (a.trunc) {
+      conv1d_tiles_kernel<DT, M, MU, P, true><<<grid, 128, 0, a.st>>>(
+          (const typename Tr::T*)a.x, (const typename Tr::T*)a.h, a.T, *a.xp, (typename Tr::T*)a.y, vec);
+      return;
+    }
+  }
+  conv1d_tiles_kernel<DT, M, MU, P, false><<<grid, 128, 0, a.st>>>(
       (const typename Tr::T*)a.x, (const typename Tr::T*)a.h, a.T, *a.xp, (typename Tr::T*)a.y, vec);
 }
 using C1Fn = void (*)(const C1Args&);
@@ -239,15 +249,16 @@ template <int DT, int M, int MU>
 __global__ void __launch_bounds__(256) conv2d_tiles_paper_kernel(const typename DType<DT>::T* __restrict__ d,
                                                                  const typename DType<DT>::T* __restrict__ g, int C,
                                                                  int64_t S, const __grid_constant__ XformParams xp,
-                                                                 int csum, int acc32,
+                                                                 int csum, int acc32, int trunc,
                                                                  typename DType<DT>::T* __restrict__ y) {
   using Tr = DType<DT>;
   constexpr int NX = M + 2;
+  const RdMode<DT> R{trunc != 0};
   __shared__ float sd[NX * NX], sg[9], sm[MU * MU];
   const int64_t s = blockIdx.x;
   const int pt = threadIdx.x, i = pt / MU, j = pt % MU;
   const bool live = pt < MU * MU;
-  auto rdadd = [&](float a, float b) { return acc32 ? __fadd_rn(a, b) : Tr::rd(__fadd_rn(a, b)); };
+  auto rdadd = [&](float a, float b) { return acc32 ? __fadd_rn(a, b) : R.rd(__fadd_rn(a, b)); };
   float stack[24];
   float msum = 0.f;
   for (int c = 0; c < C; ++c) {
@@ -261,25 +272,25 @@ __global__ void __launch_bounds__(256) conv2d_tiles_paper_kernel(const typename 
     float U1[3];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      float t = Tr::rd(__fmul_rn(Tr::rd(xp.G[i][0]), sg[0 * 3 + b]));
+      float t = R.rd(__fmul_rn(R.rd(xp.G[i][0]), sg[0 * 3 + b]));
 #pragma unroll
-      for (int a = 1; a < 3; ++a) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.G[i][a]), sg[a * 3 + b]))));
+      for (int a = 1; a < 3; ++a) t = R.rd(__fadd_rn(t, R.rd(__fmul_rn(R.rd(xp.G[i][a]), sg[a * 3 + b]))));
       U1[b] = t;
     }
-    float u = Tr::rd(__fmul_rn(Tr::rd(xp.G[j][0]), U1[0]));
+    float u = R.rd(__fmul_rn(R.rd(xp.G[j][0]), U1[0]));
 #pragma unroll
-    for (int b = 1; b < 3; ++b) u = Tr::rd(__fadd_rn(u, Tr::rd(__fmul_rn(Tr::rd(xp.G[j][b]), U1[b]))));
+    for (int b = 1; b < 3; ++b) u = R.rd(__fadd_rn(u, R.rd(__fmul_rn(R.rd(xp.G[j][b]), U1[b]))));
     // V[i][j] = sum_b BT[j][b] V1[i][b],  V1[i][b] = sum_a BT[i][a] d[a][b]
     float v = 0.f;
 #pragma unroll
     for (int b = 0; b < NX; ++b) {
-      float t = Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][0]), sd[0 * NX + b]));
+      float t = R.rd(__fmul_rn(R.rd(xp.BT[i][0]), sd[0 * NX + b]));
 #pragma unroll
-      for (int a = 1; a < NX; ++a) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.BT[i][a]), sd[a * NX + b]))));
-      const float term = Tr::rd(__fmul_rn(Tr::rd(xp.BT[j][b]), t));
-      v = b == 0 ? term : Tr::rd(__fadd_rn(v, term));
+      for (int a = 1; a < NX; ++a) t = R.rd(__fadd_rn(t, R.rd(__fmul_rn(R.rd(xp.BT[i][a]), sd[a * NX + b]))));
+      const float term = R.rd(__fmul_rn(R.rd(xp.BT[j][b]), t));
+      v = b == 0 ? term : R.rd(__fadd_rn(v, term));
     }
-    const float pc = Tr::rd(__fmul_rn(u, v));
+    const float pc = R.rd(__fmul_rn(u, v));
     if (csum == 0) {
       msum = c == 0 ? pc : rdadd(msum, pc);
     } else {
@@ -299,7 +310,7 @@ __global__ void __launch_bounds__(256) conv2d_tiles_paper_kernel(const typename 
           first = false;
         }
     }
-    sm[pt] = acc32 ? Tr::rd(msum) : msum;
+    sm[pt] = acc32 ? R.rd(msum) : msum;
   }
   __syncthreads();
   if (pt < M * M) {
@@ -308,13 +319,13 @@ __global__ void __launch_bounds__(256) conv2d_tiles_paper_kernel(const typename 
     float out = 0.f;
 #pragma unroll
     for (int jj = 0; jj < MU; ++jj) {
-      float t = Tr::rd(__fmul_rn(Tr::rd(xp.AT[p][0]), sm[0 * MU + jj]));
+      float t = R.rd(__fmul_rn(R.rd(xp.AT[p][0]), sm[0 * MU + jj]));
 #pragma unroll
-      for (int ii = 1; ii < MU; ++ii) t = Tr::rd(__fadd_rn(t, Tr::rd(__fmul_rn(Tr::rd(xp.AT[p][ii]), sm[ii * MU + jj]))));
-      const float term = Tr::rd(__fmul_rn(Tr::rd(xp.AT[q][jj]), t));
-      out = jj == 0 ? term : Tr::rd(__fadd_rn(out, term));
+      for (int ii = 1; ii < MU; ++ii) t = R.rd(__fadd_rn(t, R.rd(__fmul_rn(R.rd(xp.AT[p][ii]), sm[ii * MU + jj]))));
+      const float term = R.rd(__fmul_rn(R.rd(xp.AT[q][jj]), t));
+      out = jj == 0 ? term : R.rd(__fadd_rn(out, term));
     }
-    y[s * M * M + pt] = Tr::cvt(out);
+    y[s * M * M + pt] = R.cvt(out);
   }
 }
 
@@ -323,7 +334,7 @@ struct C2Args {
   int C;
   int64_t S;
   const XformParams* xp;
-  int csum, acc;
+  int csum, acc, trunc;
   void* y;
   cudaStream_t st;
 };
@@ -332,7 +343,7 @@ static void launch_c2(const C2Args& a) {
   using TT = typename DType<DT>::T;
   const int thr = (MU * MU + 31) / 32 * 32;
   conv2d_tiles_paper_kernel<DT, M, MU><<<(unsigned)a.S, thr, 0, a.st>>>((const TT*)a.d, (const TT*)a.g, a.C, a.S,
-                                                                       *a.xp, a.csum, a.acc, (TT*)a.y);
+                                                                       *a.xp, a.csum, a.acc, a.trunc, (TT*)a.y);
 }
 using C2Fn = void (*)(const C2Args&);
 #define C2ROW(DT, M) {&launch_c2<DT, M, M + 2>, &launch_c2<DT, M, M + 3>, &launch_c2<DT, M, M + 4>}
@@ -477,16 +488,18 @@ wino_status wino_conv1d_tiles(const void* x, const void* h, int64_t T, const win
   if (dm < 0 || dm > 2) return set_last_error("1D tiles: mu must be in [m+2, m+4]"), WINO_E_UNSUPPORTED;
   if (al->m > 8) return set_last_error("1D tiles: m <= 8 only"), WINO_E_UNSUPPORTED;
   if (T == 0) return WINO_OK;
-  C1Args a{x, h, T, &al->xp, y, reinterpret_cast<cudaStream_t>(stream)};
-  kC1[per_op_rounding ? 1 : 0][dt][al->m - 2][dm](a);
+  if (per_op_rounding & ~3) return set_last_error("1D tiles: per_op_rounding flags are bits 0 and 1"), WINO_E_ARG;
+  C1Args a{x, h, T, &al->xp, y, reinterpret_cast<cudaStream_t>(stream), (per_op_rounding & 2) ? 1 : 0};
+  kC1[(per_op_rounding & 1) ? 1 : 0][dt][al->m - 2][dm](a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
 }
 
 wino_status wino_conv2d_tiles_paper(const void* d, const void* g, int C, int64_t S, const wino_algo* al,
-                                   wino_dtype dt, int csum, int acc, void* y, void* stream) {
+                                   wino_dtype dt, int csum, int acc, int bf16_trunc, void* y, void* stream) {
   reset_launch_count();
-  if (!al || !d || !g || !y || C <= 0 || S < 0 || (csum != 0 && csum != 1) || (acc != 0 && acc != 1))
+  if (!al || !d || !g || !y || C <= 0 || S < 0 || (csum != 0 && csum != 1) || (acc != 0 && acc != 1) ||
+      (bf16_trunc != 0 && bf16_trunc != 1))
     return set_last_error("bad argument"), WINO_E_ARG;
   if (dt != WINO_F32 && dt != WINO_F16 && dt != WINO_BF16) return set_last_error("bad dtype"), WINO_E_ARG;
   if (al->lowering != WINO_LOWER_SUBSOLVER) return set_last_error("2D paper tiles: SUBSOLVER algos only"), WINO_E_UNSUPPORTED;
@@ -494,7 +507,7 @@ wino_status wino_conv2d_tiles_paper(const void* d, const void* g, int C, int64_t
   if (dm < 0 || dm > 2 || al->m > 8) return set_last_error("2D paper tiles: m <= 8, mu in [m+2, m+4]"), WINO_E_UNSUPPORTED;
   if (S > 0x7fffffff) return set_last_error("2D paper tiles: S < 2^31"), WINO_E_UNSUPPORTED;
   if (S == 0) return WINO_OK;
-  C2Args a{d, g, C, S, &al->xp, csum, acc, y, reinterpret_cast<cudaStream_t>(stream)};
+  C2Args a{d, g, C, S, &al->xp, csum, acc, bf16_trunc, y, reinterpret_cast<cudaStream_t>(stream)};
   kC2[dt][al->m - 2][dm](a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;

@@ -120,6 +120,31 @@ def main():
                      "frac_compulsory": fr["frac_compulsory"], "frac_staged": fr["frac_staged"],
                      "mean_rel": s["mean_rel"], "rel_l1": s["rel_l1"]})
     out["cfg3"] = {"workload": "N=32, C=K=256, 56x56, pad 1, fp16, post-ReLU x, He w", "rows": rows}
+
+    # ------------------------------------------------------------------ residue lowering vs sub-solver (cfg5)
+    rows = []
+    N, C, K, H, W = 256, 512, 512, 28, 28
+    x64, w64 = datagen.layer(N, C, K, H, W, "bf16", seed=0, xdist="relu_normal")
+    x = torch.from_numpy(x64).to(torch.bfloat16).cuda()
+    w = torch.from_numpy(w64).to(torch.bfloat16).cuda()
+    del x64
+    yref = Wn.wino_direct_conv2d_f64(x, w, 1, stream=st)
+    for name in ("sup1_4", "sup1_6", "sup1_8", "sup2_6"):
+        spec, m = canonical_spec(name)
+        for low in ("subsolver", "residue"):
+            algo = Wn.WinoAlgo(spec, m, lowering=low)
+            y = torch.empty((N, K, H, W), dtype=torch.bfloat16, device="cuda")
+            ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, N, C, H, W, K, 1, "bf16"))
+            step = lambda: Wn.wino_conv2d(x, w, algo, out=y, workspace=ws, stream=st)   # noqa: E731
+            for _ in range(3):
+                step()
+            ms = events_ms(step, 20, st)
+            s = Wn.summary(Wn.wino_error_stats(y, yref, m, stream=st).cpu())
+            rows.append({"algo": name, "lowering": low, "domain": algo.domain, "gemm_units": algo.units, "ms": ms,
+                         "tflops_direct_eq": bench.direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12,
+                         "mean_rel": s["mean_rel"]})
+            del ws, y
+    out["residue_vs_subsolver"] = {"workload": "cfg5 (N=256, C=K=512, 28x28) bf16", "rows": rows}
     print(json.dumps(out, indent=1))
 
 

@@ -9,6 +9,9 @@ the multiplication ratio (1D mu/n, 2D mu^2/n^2).
   point set (paired).
 * Error = mean per-trial Euclidean norm of (y - y_fp64), plus the mean relative error.
 * 1D: K5 (wino_conv1d_tiles) in the paper's per-op rounding.
+* bf16 paper-mode rows appear twice: round-to-nearest-even ("bf16") and truncation ("bf16-trunc",
+  reading A10's switch: the paper calls bf16 "a truncated form of fp32", P:6); inputs are RNE
+  bf16 values in both.
 * 2D, paper mode: K7 (wino_conv2d_tiles_paper), per-op rounding as the paper simulated it.
 * 2D, pipeline mode (the tensor-core layer): the whole layer (wino_conv2d) on batches of 64
   one-channel tiles against 64 kernels, keeping the diagonal (tile i, kernel i) pairs, so each
@@ -127,6 +130,20 @@ def run(trials, dtypes=("fp32", "fp16", "bf16"), ns=range(2, 9), seed=0, pipelin
                 rows.append({"dim": 2, "mode": "paper", "family": fam, "spec": spec, "n": n, "mu": algo.mu,
                              "dtype": dt, "ratio": algo.mu ** 2 / n ** 2, "mean_euclid": e, "mean_rel": r,
                              "nonfinite": nf})
+                if dt == "bf16":
+                    # the paper's "truncated form of fp32" read as a rounding mode (reading A10's switch)
+                    y1t = Wn.wino_conv1d_tiles(torch.from_numpy(x1d).to(td[dt]).cuda(),
+                                               torch.from_numpy(h1d).to(td[dt]).cuda(), algo, per_op_rounding=True,
+                                               bf16_mode="trunc")
+                    e, r, nf = errs(y1t.double().cpu().numpy(), ref1)
+                    rows.append({"dim": 1, "mode": "paper", "family": fam, "spec": spec, "n": n, "mu": algo.mu,
+                                 "dtype": "bf16-trunc", "ratio": algo.mu / n, "mean_euclid": e, "mean_rel": r,
+                                 "nonfinite": nf})
+                    y2t = Wn.wino_conv2d_tiles_paper(dt_d, dt_g, algo, bf16_mode="trunc")
+                    e, r, nf = errs(y2t.double().cpu().numpy(), ref2)
+                    rows.append({"dim": 2, "mode": "paper", "family": fam, "spec": spec, "n": n, "mu": algo.mu,
+                                 "dtype": "bf16-trunc", "ratio": algo.mu ** 2 / n ** 2, "mean_euclid": e,
+                                 "mean_rel": r, "nonfinite": nf})
                 if pipeline:
                     e, r, nf = errs(pipeline_diag(Wn, algo, d2d, g2d, td[dt]), ref2)
                     rows.append({"dim": 2, "mode": "pipeline", "family": fam, "spec": spec, "n": n, "mu": algo.mu,

@@ -13,7 +13,7 @@ classifier (25088 -> 1000, fp64), and its argmax is compared with the same
 network run with fp64 direct convolutions (and, as a baseline for what any
 bf16 pipeline loses, with bf16 cuDNN direct convolutions).
 
-    python scripts/vgg16_stack.py [--n 64] [--algos lin4,sup1_4,lin6,sup1_6] > profiles/vgg16_stack_r01.json
+    python scripts/vgg16_stack.py [--n 64] [--algos lin4,sup1_4,lin6,sup1_6] > profiles/vgg16_stack_r02.json
 """
 import argparse
 import json
@@ -38,9 +38,11 @@ def main():
     a = ap.parse_args()
     import numpy as np
     import torch
+    import bench
     import datagen
     import paper_1905_05233_b200 as Wn
     from paper_1905_05233_b200.algos import canonical_spec
+    peaks, peak_src = bench.load_peaks()
     dt = a.dtype
     tdt = {"bf16": torch.bfloat16, "fp16": torch.float16}[dt]
     rng = np.random.default_rng(0)
@@ -52,7 +54,10 @@ def main():
             w = rng.normal(0.0, datagen.he_sigma(cin), (cout, cin, 3, 3))
             weights.append(torch.from_numpy(w).to(tdt).cuda())
     out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, {dt}, "
-                       f"error on {a.sample} images vs fp64 direct", "algos": {}}
+                       f"error on {a.sample} images vs fp64 direct", "peaks": peak_src,
+           "roofline_note": "per layer: frac_compulsory = max(GEMM flops / tensor peak, (x + w + y) bytes / HBM) / "
+                            "time; frac_staged adds U, V and the fp32 M written and read (this design); the GEMM "
+                            "flops count the channels padded to the 64-channel block (C = 3 -> 64)", "algos": {}}
     st = torch.cuda.current_stream()
     finals = {}
     for name in a.algos.split(","):
@@ -83,7 +88,12 @@ def main():
             yref = Wn.wino_direct_conv2d_f64(xs, w, 1, stream=st)
             s = Wn.summary(Wn.wino_error_stats(y[:a.sample].contiguous(), yref, m, stream=st).cpu())
             flops = 2.0 * N * K * C * 9 * H * W
+            g = Wn.geometry(algo, N, C, H, W, K, 1, dt)
+            B = bench.layer_bytes(N, C, K, H, W, 2, g)
+            fr = bench.layer_fracs(ms, B, 2.0 * g["T"] * g["Cp"] * K * g["S"], dt, peaks)
             rows.append({"layer": li + 1, "C": C, "K": K, "HW": H, "ms": ms, "tflops_direct_eq": flops / ms / 1e9,
+                         "frac_compulsory": fr["frac_compulsory"], "frac_staged": fr["frac_staged"],
+                         "t_roof_us": fr["t_roof_us"], "t_staged_us": fr["t_staged_us"],
                          "rel_l1": s["rel_l1"], "mean_rel": s["mean_rel"], "nonfinite": s["nonfinite"]})
             del ws, yref
             act = torch.relu(y)

@@ -350,12 +350,13 @@ def test_conv1d_paper_mode_bitwise(dtype, fam, n):
     a = W.WinoAlgo(T.moduli_spec(mods), m)
     Tn = (1 << 15) + 3
     x, h = datagen.tiles1d(Tn, n, dtype, seed=n)
-    y = W.wino_conv1d_tiles(dev(x, dtype), dev(h, dtype), a, per_op_rounding=True)
-    torch.cuda.synchronize()
-    yo = P.paper_conv1d(ts, x, h, dtype)
-    g = host(y).astype(np.float32)
-    same = (g.view(np.uint32) == yo.astype(np.float32).view(np.uint32)) | (np.isnan(g) & np.isnan(yo))
-    assert same.all(), int((~same).sum())
+    for mode in (("rne", "trunc") if dtype == "bf16" else ("rne",)):
+        y = W.wino_conv1d_tiles(dev(x, dtype), dev(h, dtype), a, per_op_rounding=True, bf16_mode=mode)
+        torch.cuda.synchronize()
+        yo = P.paper_conv1d(ts, x, h, dtype, bf16_mode=mode)
+        g = host(y).astype(np.float32)
+        same = (g.view(np.uint32) == yo.astype(np.float32).view(np.uint32)) | (np.isnan(g) & np.isnan(yo))
+        assert same.all(), (mode, int((~same).sum()))
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
@@ -702,10 +703,11 @@ def test_conv2d_tiles_paper_bitwise(dtype, name, C):
     dd, gd = dev(d, dtype), dev(g, dtype)
     for csum in ("sequential", "pairwise"):
         for acc in ("dtype", "fp32"):
-            y = host(W.wino_conv2d_tiles_paper(dd, gd, a, csum, acc)).astype(np.float32)
-            yo = P.paper_conv2d_tiles(ts, d, g, dtype, csum=csum, acc=acc).astype(np.float32)
-            same = (y.view(np.uint32) == yo.view(np.uint32)) | (np.isnan(y) & np.isnan(yo))
-            assert same.all(), (csum, acc, int((~same).sum()))
+            for mode in (("rne", "trunc") if dtype == "bf16" else ("rne",)):
+                y = host(W.wino_conv2d_tiles_paper(dd, gd, a, csum, acc, bf16_mode=mode)).astype(np.float32)
+                yo = P.paper_conv2d_tiles(ts, d, g, dtype, bf16_mode=mode, csum=csum, acc=acc).astype(np.float32)
+                same = (y.view(np.uint32) == yo.view(np.uint32)) | (np.isnan(y) & np.isnan(yo))
+                assert same.all(), (csum, acc, mode, int((~same).sum()))
 
 
 @pytest.mark.parametrize("name,dtype", [("lin8", "fp16"), ("lin8", "bf16"), ("lin6", "fp16"), ("sup1_8", "fp16")])
