@@ -34,17 +34,36 @@ def _flags(src):
     return ["-x", "c++"] + common
 
 
-def _deps():
-    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(HERE, "..", "include", "wino.h")]
+def _deps(src):
+    """src and the local headers it includes (transitively): an edit to one
+    kernel file rebuilds only the objects that see it."""
+    inc = [CSRC, os.path.join(HERE, "..", "include")]
+    seen, todo = set(), [os.path.join(CSRC, src)]
+    while todo:
+        f = todo.pop()
+        if f in seen:
+            continue
+        seen.add(f)
+        with open(f) as fh:
+            for line in fh:
+                line = line.strip()
+                if line.startswith("#include") and '"' in line:
+                    name = line.split('"')[1]
+                    for d in [os.path.dirname(f)] + inc:
+                        c = os.path.normpath(os.path.join(d, name))
+                        if os.path.exists(c):
+                            todo.append(c)
+                            break
+    return sorted(seen)
 
 
 def build(force=False, jobs=None, verbose=False):
     os.makedirs(OBJ, exist_ok=True)
-    dep_mtime = max(os.path.getmtime(p) for p in _deps())
     objs, todo = [], []
     for s in SOURCES:
         o = os.path.join(OBJ, s + ".o")
         objs.append(o)
+        dep_mtime = max(os.path.getmtime(p) for p in _deps(s))
         if force or not os.path.exists(o) or os.path.getmtime(o) < dep_mtime:
             todo.append((s, o))
 

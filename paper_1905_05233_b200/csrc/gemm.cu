@@ -24,6 +24,7 @@
 //               (cp.async.bulk.tensor, clipped at the ragged edges).  The
 //               accumulator is released to the MMA warp as soon as its last
 //               columns are in registers.
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -177,8 +178,248 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA-pair variant
+// The same GEMM with cta_group::2: a cluster of two CTAs (one TPC) owns a
+// [256 t x 256 k] output tile of one point.  CTA r loads its own A block (V, tiles
+// [256 mb2 + 128 r, +128)) and half of B (U rows k in [256 nb + 128 r, +128)); the
+// leader's single MMA thread issues M = 256, N = 256 MMAs that read both CTAs'
+// shared memory, and each CTA's TMEM receives its own 128 tile rows x 256 k.
+// Per SM that is 32 KB of operands per 128 x 256 x 64 step instead of 48 KB
+// (B is no longer loaded by both SMs): K3 at one CTA per SM is bound by the
+// SM's L2 ingress together with its fp32 M egress.
+//   barriers: full[s] (leader: 2 arrivals + both CTAs' bytes), empty[s] (each CTA,
+//   multicast MMA commit), tfull[a] (each CTA, multicast commit), tempty[a]
+//   (leader: 4 epilogue warps x 2 CTAs, remote arrives from the peer).
+template <bool kTF32, int STAGES, int EPI, int EC = 32>
+struct PairCfg {
+  static constexpr int ES = kTF32 ? 4 : 2;
+  static constexpr int BK = 128 / ES;
+  static constexpr int UK = kTF32 ? 8 : 16;
+  static constexpr int NPL = kTF32 ? 2 : 1;
+  static constexpr int BN = 256;                    // k per pair tile (N of the MMA)
+  static constexpr int A_BYTES = kBM * 128;         // 128 t rows x 128 B
+  static constexpr int B_BYTES = (BN / 2) * 128;    // this CTA's 128 k rows
+  static constexpr int STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int EPI_COLS = EC;               // k columns per M store box
+  static constexpr int EPI_BYTES = EC * kBM * 4;
+  static constexpr int EPI_BUFS = EPI;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_BUFS * EPI_BYTES + 1024 + 256;
+  static_assert(EPI_BUFS >= 2 && SMEM <= 227 * 1024 && (EC == 16 || EC == 32), "shared memory");
+};
+
+// L2 eviction-priority policy (createpolicy) for the streamed fp32 M stores
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                                  uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+
+template <bool kTF32, int STAGES, int EPI, bool kHint, int EC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    domain_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                            const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB2, int nNB, int Q,
+                            int S, uint32_t idesc, const __grid_constant__ GemmSched gs, int mb0, int TBv) {
+  using Cfg = PairCfg<kTF32, STAGES, EPI, EC>;
+  constexpr int BN = Cfg::BN;
+  extern __shared__ uint8_t smem_raw[];
+  // the same offset in both CTAs (the MMA addresses the peer's operands by the leader's offsets)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmM);
+    // full: (leader) its own expect_tx arrival + the peer's arrival, both CTAs' bytes;
+    // tempty: (leader) 4 epilogue warps x 2 CTAs
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 8);
+    fence_barrier_init();
+    fence_proxy_async_shared();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int nItems = Q * nMB2 * nNB;
+  const int KB = Cp / Cfg::BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int item = cl; item < nItems; item += ncl) {
+        const int nb = item % nNB, mb2 = (item / nNB) % nMB2, p = item / (nNB * nMB2);
+        const int mb = mb0 + 2 * mb2 + (int)rank;   // this CTA's 128-tile block
+        const int k0 = nb * BN + (int)rank * (BN / 2);
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          const int qi = gs.in_pt[pr], sl = gs.slab[pr];
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t fb = mapa_rank(&full[stage], 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            else mbar_arrive_cluster(fb);
+            uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
+            tma_load_3d_pair(base, &tmV, fb, 0, 0, (mb * KB + kb) * Q + qi);
+            if constexpr (kTF32) tma_load_3d_pair(base + Cfg::A_BYTES, &tmV, fb, 0, 0, ((TBv + mb) * KB + kb) * Q + qi);
+            uint8_t* bb = base + Cfg::NPL * Cfg::A_BYTES;
+            tma_load_3d_pair(bb, &tmU, fb, kb * Cfg::BK, k0, sl);
+            if constexpr (kTF32) tma_load_3d_pair(bb + Cfg::B_BYTES, &tmU, fb, kb * Cfg::BK, k0, sl + S);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+      }
+      // drain: every stage released by the leader's MMAs (all multicast arrivals
+      // on this CTA's barriers have landed before the CTA may exit)
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) stage = 0, phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int item = cl; item < nItems; item += ncl) {
+        const int p = item / (nNB * nMB2);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        int step = 0;
+        for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
+          for (int kb = 0; kb < KB; ++kb, ++step) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+            const uint32_t b0 = a0 + Cfg::NPL * Cfg::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint32_t koff = k * Cfg::UK * Cfg::ES;  // 32 bytes
+              mma_ss_pair<kTF32>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc,
+                                 (step | k) != 0);
+              if constexpr (kTF32) {
+                mma_ss_pair<true>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + Cfg::B_BYTES + koff),
+                                  idesc, 1);
+                mma_ss_pair<true>(d_tmem, umma_desc_sw128(a0 + Cfg::A_BYTES + koff), umma_desc_sw128(b0 + koff),
+                                  idesc, 1);
+              }
+            }
+            mma_commit_pair(&empty[stage]);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+        mma_commit_pair(&tfull[acc]);
+        if (++acc == 2) acc = 0, acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue (both CTAs)
+    const int wq = warp & 3;
+    const bool storer = (warp == 4 && lane == 0);
+    uint64_t pol = 0;
+    if constexpr (kHint) pol = l2_evict_first();
+    int acc = 0, chunk = 0;
+    uint32_t acc_phase = 0;
+    for (int item = cl; item < nItems; item += ncl) {
+      const int nb = item % nNB, mb2 = (item / nNB) % nMB2, p = item / (nNB * nMB2);
+      const int t0 = (2 * mb2 + (int)rank) * kBM;   // relative to mb0 * 128 (M holds this slice)
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
+        if (j0 + 32 == BN) {  // accumulator fully read: hand it back to the leader's MMA thread
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+        }
+        if (nb * BN + j0 >= K || t0 >= T) continue;   // columns past K, tile block past the slice (uniform)
+#pragma unroll
+        for (int h = 0; h < 32; h += EC) {
+          float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
+          if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int jj = 0; jj < EC; ++jj) buf[jj * kBM + wq * 32 + lane] = v[h + jj];
+          fence_proxy_async_shared();
+          named_bar_sync(1, 128);
+          if (storer) {
+            if constexpr (kHint) tma_store_3d_hint(&tmM, buf, t0, nb * BN + j0 + h, p, pol);
+            else tma_store_3d(&tmM, buf, t0, nb * BN + j0 + h, p);
+            bulk_commit();
+          }
+          ++chunk;
+        }
+      }
+      if (++acc == 2) acc = 0, acc_phase ^= 1;
+    }
+    if (storer) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
+template <bool kTF32, int STAGES, int EPI, bool kHint, int EC = 32>
+static wino_status launch_gemm_pair(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
+                                    const GemmSched& gs, uint32_t fmt, int mb0, int nT, cudaStream_t st) {
+  using Cfg = PairCfg<kTF32, STAGES, EPI, EC>;
+  auto kern = domain_gemm_pair_kernel<kTF32, STAGES, EPI, kHint, EC>;
+  WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int nMB2 = (nT + 2 * kBM - 1) / (2 * kBM), nNB = (g.K + Cfg::BN - 1) / Cfg::BN;
+  const int items = g.Q * nMB2 * nNB;
+  DevState* ds = dev_state();
+  if (!ds) return WINO_E_CUDA;
+  if (ds->pair_clusters == 0) {   // co-resident clusters of two (every config runs one CTA per SM)
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(2 * (ds->sms / 2), 1, 1);
+    qc.blockDim = dim3(256, 1, 1);
+    qc.dynamicSmemBytes = Cfg::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    qc.attrs = at, qc.numAttrs = 1;
+    int ncl = 0;
+    WINO_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, kern, &qc));
+    ds->pair_clusters = ncl > 0 ? ncl : 1;
+  }
+  const int ncl = items < ds->pair_clusters ? items : ds->pair_clusters;
+  kern<<<2 * ncl, 256, Cfg::SMEM, st>>>(tv, tu, tm, nT, g.K, g.Cp, nMB2, nNB, g.Q, g.S,
+                                        make_idesc(fmt, 2 * kBM, Cfg::BN), gs, mb0, g.TB);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
 
 template <bool kTF32, int BN, int STAGES>
 static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
@@ -194,6 +435,13 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
                                      make_idesc(fmt, kBM, BN), gs, mb0, g.TB);
   WINO_LAUNCH_CHECK();
   return WINO_OK;
+}
+
+// The CTA-pair K3 is the default for 16-bit layers with K > 128 (WINO_PAIR=0 selects
+// the one-CTA kernel, for comparison).
+static bool pair_enabled() {
+  const char* e = getenv("WINO_PAIR");   // read per call (tests compare both kernels in one process)
+  return !(e && *e == '0');
 }
 
 // M_xi for the tiles [mb0 * 128, mb0 * 128 + nT) of V (all of them by default) into
@@ -218,8 +466,26 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
   // UMMA operand formats: kind::f16 F16 = 0, BF16 = 1; kind::tf32 TF32 = 2.
   const uint32_t fmt = dt == WINO_F16 ? 0u : dt == WINO_BF16 ? 1u : 2u;
   if (tf32) {
+    if (g.K > 128 && nT > kBM && pair_enabled()) {
+      CUtensorMap tu2;
+      if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {
+        set_last_error("cuTensorMapEncodeTiled failed");
+        return WINO_E_CUDA;
+      }
+      return launch_gemm_pair<true, 3, 2, false>(tv, tu2, tm, g, al->gs, fmt, mb0, nT, st);
+    }
     if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
     return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+  }
+  if (BN == 256 && nT > kBM && pair_enabled()) {
+    CUtensorMap tu2;   // B boxes of 128 k rows: each CTA of the pair loads half of the 256-wide tile
+    if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {
+      set_last_error("cuTensorMapEncodeTiled failed");
+      return WINO_E_CUDA;
+    }
+    // 6 stages + 2 epilogue buffers: 237 us on cfg5 lin4 bf16 (5 + 4: 248; 4 + 6: 262;
+    // 3 + 8: 296; 16-column store boxes or an evict-first L2 hint on the M stores: +-2)
+    return launch_gemm_pair<false, 6, 2, false>(tv, tu2, tm, g, al->gs, fmt, mb0, nT, st);
   }
   if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);   // 3 stages + 4 epilogue buffers: 8 % slower
   if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);

@@ -125,7 +125,10 @@ def test_input_transform(dtype, name, lowering, pad, shape):
 @pytest.mark.parametrize("name,lowering,T_,C,K", [("lin4", "subsolver", 300, 136, 72),
                                                   ("lin2", "subsolver", 129, 64, 256),
                                                   ("sup1_4", "residue", 257, 70, 40),
-                                                  ("lin4", "subsolver", 1000, 512, 512)])
+                                                  ("lin4", "subsolver", 1000, 512, 512),
+                                                  # CTA-pair K3 (K > 128): odd tile-block count, half-empty k tile
+                                                  ("lin4", "subsolver", 300, 136, 384),
+                                                  ("sup1_4", "residue", 383, 70, 200)])
 def test_domain_gemm_isolated(dtype, name, lowering, T_, C, K):
     """Feed identical U, V (oracle-made, dtype values) to the tensor-core GEMM."""
     a, ref, m = algo_pair(name, lowering)
@@ -156,6 +159,42 @@ def test_domain_gemm_isolated(dtype, name, lowering, T_, C, K):
     # fp32 accumulation of exact products: |err| <= gamma_n * sum |u v|
     n = C * max(1, S // Q)
     assert (np.abs(got - want) <= 1.01 * n * 2.0 ** -24 * aw + 1e-30).all()
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("T_,K", [(300, 384), (1000, 512), (129, 256)])
+def test_domain_gemm_pair_equals_single(dtype, T_, K, monkeypatch):
+    """The CTA-pair K3 (cta_group::2, default for K > 128) and the one-CTA kernel
+    (WINO_PAIR=0) run the same fp32 accumulation: identical bits."""
+    a, ref, m = algo_pair("lin4")
+    rng = np.random.default_rng(11)
+    Q, C = a.domain ** 2, 200
+    Cp = -(-C // 64) * 64
+    Vh = np.zeros((1, Q, T_, Cp))
+    Uh = np.zeros((1, Q, K, Cp))
+    Vh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, T_, C)), dtype)
+    Uh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, K, C)), dtype)
+    Vd, Ud = W.v_from_dense(dev(Vh, dtype)), dev(Uh, dtype)
+    M2 = W.wino_domain_gemm(Vd, Ud, a, C, K, T_)
+    monkeypatch.setenv("WINO_PAIR", "0")
+    M1 = W.wino_domain_gemm(Vd, Ud, a, C, K, T_)
+    torch.cuda.synchronize()
+    assert torch.equal(M1[:, :, :T_], M2[:, :, :T_])
+
+
+def test_domain_gemm_pair_equals_single_tf32(monkeypatch):
+    """fp32 (3xTF32 from hi/lo planes): the CTA-pair K3 equals the one-CTA kernel bitwise."""
+    a, ref, m = algo_pair("lin4")
+    x, w = datagen.layer(3, 96, 200, 22, 26, "fp32", seed=6)
+    U = W.wino_weight_transform(dev(w, "fp32"), a)
+    V = W.wino_input_transform(dev(x, "fp32"), a)
+    T_all = CV.tile_grid(22, 26, 4, 1)
+    T0 = 3 * T_all[2] * T_all[3]
+    M2 = W.wino_domain_gemm(V, U, a, 96, 200, T0)
+    monkeypatch.setenv("WINO_PAIR", "0")
+    M1 = W.wino_domain_gemm(V, U, a, 96, 200, T0)
+    torch.cuda.synchronize()
+    assert torch.equal(M1[:, :, :T0], M2[:, :, :T0])
 
 
 def test_domain_gemm_tf32x3():
