@@ -100,6 +100,14 @@ __device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair_hint(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                      int c1, int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+      "[%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_4d_hint(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
                                                   int c3, uint64_t pol) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3, %4, %5}], [%1], %6;" ::"l"(
@@ -180,88 +188,104 @@ __device__ __forceinline__ void split_xform(const Src& m, const SplitArgs& sa, i
 // then released before the math), else 1
 __host__ __device__ constexpr int split_nc(int Q) { return 2 * Q <= 80 ? 2 : 1; }
 
-template <int BN, int STAGES, int DT, int MO, int DO>
+// GEMM role: the CTA-pair pipeline of gemm.cu (domain_gemm_pair_kernel): a cluster of
+// two CTAs owns a [256 t x 256 k] tile of one point; CTA r stores its 128 tiles.
+template <int STAGES, int EPI, int DT, int MO, int DO>
 __global__ void __launch_bounds__(kSplitThreads, 1)
     domain_gemm_split_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                              const __grid_constant__ CUtensorMap tmMb, int Cp, uint32_t idesc,
                              const __grid_constant__ GemmSched gs, const __grid_constant__ SplitArgs sa) {
-  using Cfg = GemmCfg<false, BN, STAGES>;
+  constexpr int BN = 256;
+  constexpr int BK = 64, UK = 16, ES = 2;
+  constexpr int A_BYTES = kBM * 128, B_BYTES = (BN / 2) * 128, STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr int EPI_BYTES = 32 * kBM * 4, TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Q = sa.Q, K = sa.K;
 
   if (blockIdx.x < sa.G) {
-    // ============================================================== GEMM role
-    float* epi = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BUFS * Cfg::EPI_BYTES);
+    // ============================================================== GEMM role (CTA pairs)
+    float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES + EPI * EPI_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const uint32_t rank = cluster_ctarank();
+    const int cl = blockIdx.x >> 1, ncl = sa.G >> 1;
     if (warp == 0 && lane == 0) {
       tma_prefetch(&tmV);
       tma_prefetch(&tmU);
       tma_prefetch(&tmMb);
-      for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1), mbar_init(&empty[s], 1);
-      for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 4);
+      for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
+      for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 8);
       fence_barrier_init();
       fence_proxy_async_shared();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+    if (warp == 2) tmem_alloc_pair(tmem_slot, TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+    const int nMB2 = (sa.nMB + 1) >> 1;
     const int per_mb = Q * sa.nNB;
-    const int nItems = sa.nMB * per_mb;
-    const int KB = Cp / Cfg::BK;
-    const int G = sa.G;
-    const bool pmaj = (sa.dbg & 20) == 20;
+    const int nItems = nMB2 * per_mb;
+    const int KB = Cp / BK;
+    // mb-major order: the tile blocks finish one after the other for the transform role
+    const bool pmaj = (sa.dbg & 20) == 20;   // p-major order (the staged kernel's), GEMM-alone timing only
     auto decode = [&](int item, int& mb, int& p, int& nb) {
       if (pmaj) {
-        nb = item % sa.nNB, mb = (item / sa.nNB) % sa.nMB, p = item / (sa.nNB * sa.nMB);
-      } else {
-        mb = item / per_mb;
-        const int r = item % per_mb;
-        p = r / sa.nNB, nb = r % sa.nNB;
+        nb = item % sa.nNB, mb = 2 * ((item / sa.nNB) % nMB2) + (int)rank, p = item / (sa.nNB * nMB2);
+        return;
       }
+      mb = 2 * (item / per_mb) + (int)rank;
+      const int r = item % per_mb;
+      p = r / sa.nNB, nb = r % sa.nNB;
     };
 
     if (warp == 0) {
       if (lane == 0) {
-        // ---------------------------------------------- TMA producer (+ backpressure)
+        // ---------------------------------------------- TMA producer (+ backpressure), both CTAs
         int stage = 0, held = -1;
         uint32_t phase = 0;
-        for (int item = blockIdx.x; item < nItems; item += G) {
+        for (int item = cl; item < nItems; item += ncl) {
           int mb, p, nb;
           decode(item, mb, p, nb);
-          if (sa.lag > 0 && mb >= sa.lag && held != mb) {
-            while (ld_relaxed_gpu(sa.fixed + mb - sa.lag) < K) __nanosleep(256);
-            held = mb;
+          const int mbw = mb & ~1;   // both CTAs of the pair hold back on the same block
+          if (sa.lag > 0 && mbw >= sa.lag && held != mbw) {
+            while (ld_relaxed_gpu(sa.fixed + mbw - sa.lag) < K) __nanosleep(256);
+            held = mbw;
           }
+          const int k0 = nb * BN + (int)rank * (BN / 2);
           for (int pr = gs.off[p]; pr < gs.off[p + 1]; ++pr) {
             const int qi = gs.in_pt[pr], sl = gs.slab[pr];
             for (int kb = 0; kb < KB; ++kb) {
               mbar_wait(&empty[stage], phase ^ 1);
-              mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-              uint8_t* base = smem + stage * Cfg::STAGE_BYTES;
-              if (sa.dbg & 32) tma_load_3d(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi);
-              else tma_load_3d_hint(base, &tmV, &full[stage], 0, 0, (mb * KB + kb) * Q + qi, pol_first);
-              tma_load_3d(base + Cfg::A_BYTES, &tmU, &full[stage], kb * Cfg::BK, nb * BN, sl);
+              const uint32_t fb = mapa_rank(&full[stage], 0);
+              if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+              else mbar_arrive_cluster(fb);
+              uint8_t* base = smem + stage * STAGE_BYTES;
+              if (sa.dbg & 32) tma_load_3d_pair(base, &tmV, fb, 0, 0, (mb * KB + kb) * Q + qi);
+              else tma_load_3d_pair_hint(base, &tmV, fb, 0, 0, (mb * KB + kb) * Q + qi, pol_first);
+              tma_load_3d_pair(base + A_BYTES, &tmU, fb, kb * BK, k0, sl);
               if (++stage == STAGES) stage = 0, phase ^= 1;
             }
           }
         }
+        for (int s = 0; s < STAGES; ++s) {   // drain: all multicast arrivals on this CTA have landed
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (++stage == STAGES) stage = 0, phase ^= 1;
+        }
       }
       __syncwarp();
     } else if (warp == 1) {
-      if (lane == 0) {
-        // ---------------------------------------------- MMA issuer
+      if (lane == 0 && rank == 0) {
+        // ---------------------------------------------- MMA issuer (leader)
         int stage = 0, acc = 0;
         uint32_t phase = 0, acc_phase = 0;
-        for (int item = blockIdx.x; item < nItems; item += G) {
+        for (int item = cl; item < nItems; item += ncl) {
           int mb, p, nb;
           decode(item, mb, p, nb);
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -272,18 +296,19 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
             for (int kb = 0; kb < KB; ++kb, ++step) {
               mbar_wait(&full[stage], phase);
               tc_fence_after();
-              const uint32_t a0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-              const uint32_t b0 = a0 + Cfg::A_BYTES;
+              const uint32_t a0 = smem_u32(smem + stage * STAGE_BYTES);
+              const uint32_t b0 = a0 + A_BYTES;
 #pragma unroll
-              for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
-                const uint32_t koff = k * Cfg::UK * Cfg::ES;
-                mma_ss<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc, (step | k) != 0);
+              for (int k = 0; k < BK / UK; ++k) {
+                const uint32_t koff = k * UK * ES;
+                mma_ss_pair<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc,
+                                   (step | k) != 0);
               }
-              mma_commit(&empty[stage]);
+              mma_commit_pair(&empty[stage]);
               if (++stage == STAGES) stage = 0, phase ^= 1;
             }
           }
-          mma_commit(&tfull[acc]);
+          mma_commit_pair(&tfull[acc]);
           if (++acc == 2) acc = 0, acc_phase ^= 1;
         }
       }
@@ -294,9 +319,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
       const bool storer = (warp == 4 && lane == 0);
       int acc = 0, chunk = 0, pend = -1;
       uint32_t acc_phase = 0;
-      for (int item = blockIdx.x; item < nItems; item += G) {
+      for (int item = cl; item < nItems; item += ncl) {
         int mb, p, nb;
         decode(item, mb, p, nb);
+        const bool live = mb < sa.nMB;   // the last pair's second block may lie past the layer
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         int nbox = 0;
@@ -307,11 +333,11 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
           if (j0 + 32 == BN) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
           }
-          if (nb * BN + j0 >= K) continue;
-          float* buf = epi + (chunk % Cfg::EPI_BUFS) * (Cfg::EPI_BYTES / 4);
-          if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
+          if (nb * BN + j0 >= K || !live) continue;
+          float* buf = epi + (chunk % EPI) * (EPI_BYTES / 4);
+          if (storer) bulk_wait_read<EPI - 1>();
           named_bar_sync(1, 128);
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
@@ -324,14 +350,14 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
           }
           ++chunk, ++nbox;
         }
-        if (storer && !(sa.dbg & 8)) {
+        if (storer && live && !(sa.dbg & 8)) {
           // Publish the item once its stores are complete.  To keep the epilogue
           // from draining its stores after every item, the publication of item i
-          // is deferred until item i + G's stores are issued -- unless the
-          // producer's backpressure could make item i + G wait for item i's
-          // tile block (its block is lag or more blocks later): then now.
-          const int nxt = item + G;
-          const bool defer = nxt < nItems && (sa.lag == 0 || nxt / per_mb < mb + sa.lag);
+          // is deferred until the next item's stores are issued -- unless the
+          // producer's backpressure could make that item wait for item i's tile
+          // block (its block is lag or more blocks later): then now.
+          const int nxt = item + ncl;
+          const bool defer = nxt < nItems && (sa.lag == 0 || 2 * (nxt / per_mb) < (mb & ~1) + sa.lag);
           if (pend >= 0) {   // the previous item: complete once only this item's nbox groups remain
             bulk_wait_pending(nbox);
             fence_proxy_async_global();
@@ -350,11 +376,19 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
         }
         if (++acc == 2) acc = 0, acc_phase ^= 1;
       }
+      if (storer && pend >= 0) {
+        bulk_wait_all();
+        fence_proxy_async_global();
+        __threadfence();
+        red_release_gpu_add(sa.done + pend, 1);
+      }
+      if (storer) bulk_wait_all();
     }
-    __syncthreads();
+    tc_fence_before();
+    cluster_sync_all();
     if (warp == 2) {
       tc_fence_after();
-      tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+      tmem_dealloc_pair(tmem_base, TMEM_COLS);
     }
     return;
   }
@@ -445,9 +479,10 @@ __global__ void __launch_bounds__(kSplitThreads, 1)
 template <int DT, int MO, int DO>
 static wino_status launch_split(const CUtensorMap& tv, const CUtensorMap& tu, const Geo& g, const wino_algo* al,
                                 uint32_t fmt, float* Mw, void* y, int* cnt, cudaStream_t st) {
-  constexpr int BN = 256, STAGES = 4;
-  using Cfg = GemmCfg<false, BN, STAGES>;
-  auto kern = domain_gemm_split_kernel<BN, STAGES, DT, MO, DO>;
+  constexpr int STAGES = 6, EPI = 2;   // the staged pair kernel's best configuration (gemm.cu)
+  constexpr int SMEM = STAGES * (kBM * 128 + 128 * 128) + EPI * 32 * kBM * 4 + 1024 + 256;
+  constexpr int BN = 256;
+  auto kern = domain_gemm_split_kernel<STAGES, EPI, DT, MO, DO>;
   const int nMB = g.TB, nNB = (g.K + BN - 1) / BN;
   const int Q = g.Q;
   CUtensorMap tmb;
@@ -475,9 +510,10 @@ static wino_status launch_split(const CUtensorMap& tv, const CUtensorMap& tu, co
     const double ratio = (Mbytes / 110e9) / (F / 9.5e12);   // R / G
     R = (int)(sms * ratio / (1.0 + ratio) + 0.5);
     if (const char* e = getenv("WINO_SPLIT_R")) R = atoi(e);
-    R = R < 1 ? 1 : (R > sms - 1 ? sms - 1 : R);
+    R = R < 1 ? 1 : (R > sms - 2 ? sms - 2 : R);
   }
-  sa.G = sms - R;
+  sa.G = (sms - R) & ~1;   // whole CTA pairs
+  if (sa.G < 2) sa.G = 2;
   sa.lag = 6;
   if (const char* e = getenv("WINO_SPLIT_LAG")) sa.lag = atoi(e);
   if (const char* e = getenv("WINO_SPLIT_DBG")) sa.dbg = atoi(e);
@@ -485,12 +521,12 @@ static wino_status launch_split(const CUtensorMap& tv, const CUtensorMap& tu, co
   // transform ring: slots of KP channel pieces (Q * 512 B each)
   const size_t piece_bytes = (size_t)Q * kBM * 4;
   sa.KP = split_nc(Q);
-  const size_t budget = (size_t)Cfg::SMEM - 1024 - 256;
+  const size_t budget = (size_t)SMEM - 1024 - 256;
   sa.NB = (int)(budget / (sa.KP * piece_bytes));
   if (sa.NB > 8) sa.NB = 8;
   sa.NB &= ~1;
   if (sa.NB < 2) return WINO_E_UNSUPPORTED;
-  const int smem = Cfg::SMEM;
+  const int smem = SMEM;
   WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   WINO_CUDA_CHECK(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * nMB, st));
   cudaLaunchConfig_t cfg = {};
@@ -498,12 +534,15 @@ static wino_status launch_split(const CUtensorMap& tv, const CUtensorMap& tu, co
   cfg.blockDim = dim3(kSplitThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident: the roles wait on each other
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;   // CTA pairs (the transform role ignores its peer)
+  attr[1].val.clusterDim.x = 2, attr[1].val.clusterDim.y = 1, attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const uint32_t idesc = make_idesc(fmt, kBM, BN);
+  cfg.numAttrs = 2;
+  cfg.gridDim = dim3(sms & ~1);
+  const uint32_t idesc = make_idesc(fmt, 2 * kBM, BN);
   WINO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tv, tu, tmb, g.Cp, idesc, al->gs, sa));
   WINO_LAUNCH_CHECK();
   return WINO_OK;
@@ -543,7 +582,7 @@ wino_status run_domain_gemm_split(const void* V, const void* U, const Geo& g, co
   const uint32_t BK = 128 / (uint32_t)g.es;
   CUtensorMap tv, tu;
   if (!make_map3(&tv, cdt, g.es, V, BK, kBM, (uint64_t)g.planes * g.Q * g.TB * (g.Cp / BK), BK, kBM) ||
-      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN)) {
+      !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN / 2)) {   // each CTA: half of B
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
     return WINO_E_CUDA;
   }
