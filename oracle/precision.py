@@ -17,6 +17,9 @@ PIPELINE mode (the rounding points of the staged GPU path): x and w are dtype
   values; U = rd(G g G^T), V = rd(B^T d B) computed in fp32 with fp32-lowered
   matrices; M = sum_c U V accumulated in fp32; y = rd(A^T M A) computed in fp32.
   The order of fp32 operations inside each stage is not part of the model.
+  m_store="dtype" (reading M3, the layer form of the "mixed
+  precision" booster of P:611 / reading M2): the fp32 channel sum M is rounded
+  once to the dtype before the output transform, y = rd(A^T rd(M) A).
 
 The absolute error magnitudes these models produce are "parity unpinned"
 (Figure 1 is absent from PAPER.md); their trends are pinned in tests.
@@ -144,9 +147,11 @@ def pipeline_input_transform(ts, x, dtype, pad=1, bf16_mode="rne"):
     return V, grid
 
 
-def pipeline_conv2d(ts, x, w, dtype, pad=1, bf16_mode="rne", chunk=16, return_parts=False):
+def pipeline_conv2d(ts, x, w, dtype, pad=1, bf16_mode="rne", chunk=16, return_parts=False, m_store="fp32"):
     """Whole layer in PIPELINE mode.  x: [N, C, H, W] dtype values (any float
-    array), w: [K, C, 3, 3].  Returns y as fp32 array of dtype values."""
+    array), w: [K, C, 3, 3].  Returns y as fp32 array of dtype values.
+    m_store: "fp32" (reading R1) or "dtype" (reading M3: M rounded once)."""
+    assert m_store in ("fp32", "dtype")
     x = np.asarray(x)
     N, C, H, W = x.shape
     K = w.shape[0]
@@ -160,6 +165,9 @@ def pipeline_conv2d(ts, x, w, dtype, pad=1, bf16_mode="rne", chunk=16, return_pa
         xs = x[n0:n0 + chunk]
         V, _ = pipeline_input_transform(ts, xs, dtype, pad, bf16_mode)
         Mx = np.matmul(U, V.transpose(0, 1, 3, 2))                   # (mu, mu, K, T) fp32 accumulate
+        if m_store == "dtype":
+            with np.errstate(over="ignore"):
+                Mx = rd(dtype, Mx, bf16_mode)                        # M3: one rounding of the channel sum
         Yt = rd(dtype, sep2(AT, Mx), bf16_mode)                      # (m, m, K, T)
         y[n0:n0 + chunk] = _scatter_tiles(Yt, xs.shape[0], K, th, tw, m, Ho, Wo)
         if return_parts:
@@ -215,7 +223,8 @@ def pipeline_residue_weights(rb, w, dtype, bf16_mode="rne"):
     return units, np.stack(Ws)                                        # (n_units, K, C)
 
 
-def pipeline_residue_conv2d(rb, x, w, dtype, pad=1, bf16_mode="rne", chunk=16):
+def pipeline_residue_conv2d(rb, x, w, dtype, pad=1, bf16_mode="rne", chunk=16, m_store="fp32"):
+    assert m_store in ("fp32", "dtype")
     x = np.asarray(x)
     N, C, H, W = x.shape
     K = w.shape[0]
@@ -234,6 +243,9 @@ def pipeline_residue_conv2d(rb, x, w, dtype, pad=1, bf16_mode="rne", chunk=16):
         Z = np.zeros((D * D, K, V.shape[1]), np.float32)
         for u, (po, pi, *_rest) in enumerate(units):
             Z[po] = (Z[po] + Wst[u] @ V[pi].T).astype(np.float32)
+        if m_store == "dtype":
+            with np.errstate(over="ignore"):
+                Z = rd(dtype, Z, bf16_mode)                          # M3: one rounding of the domain sum
         Yt = rd(dtype, sep2(APT, Z.reshape(D, D, K, -1)), bf16_mode)
         y[n0:n0 + chunk] = _scatter_tiles(Yt, xs.shape[0], K, th, tw, m, Ho, Wo)
     return y
@@ -372,13 +384,19 @@ def abs_bound_conv2d(ts, x, w, dtype, pad=1, C_acc=None, mma_rel=0.0):
 ETA = {"fp32": 2.0 ** -150, "fp16": 2.0 ** -25, "bf16": 2.0 ** -134, "fp64": 0.0}
 
 
-def elementwise_bound(ts, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05):
+def elementwise_bound(ts, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05, m_store="fp32"):
     """|y_pipeline - y_exact| <= (2 u_d + g) S + eta S_eta + u_d |y| + eta, with
     S_eta = |A|^T ( sum_c (|G||g||G|^T) + (|B|^T|d||B|) + eta ) |A| the
-    propagation of underflow (absolute) errors of U and V (fp16 lin8 collapse)."""
+    propagation of underflow (absolute) errors of U and V (fp16 lin8 collapse).
+    m_store="dtype" (reading M3) adds the rounding of M, |rd(M) - M| <= u_d |M|
+    + eta, propagated by |A|^T . |A|: + u_d S + eta (max_p sum_i |A_ip|)^2."""
     S, g, u_d, S_eta = _abs_bound_parts(ts, x, w, dtype, pad, None, mma_rel)
     eta = ETA[dtype]
-    return safety * ((2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta)
+    b = (2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta
+    if m_store == "dtype":
+        a1 = np.abs(np.array([[float(v) for v in r] for r in ts.AT])).sum(axis=1).max()
+        b = b + u_d * S + eta * a1 * a1
+    return safety * b
 
 
 def _abs_bound_parts(ts, x, w, dtype, pad, C_acc, mma_rel):
@@ -404,7 +422,7 @@ def _abs_bound_parts(ts, x, w, dtype, pad, C_acc, mma_rel):
     return S, g, u_d, S_eta
 
 
-def residue_elementwise_bound(rb, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05):
+def residue_elementwise_bound(rb, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=1.05, m_store="fp32"):
     """First-order forward error bound of the residue-block pipeline
     (pipeline_residue_conv2d; reading R1 applied to A3'):
         |y - y_exact| <= (2 u_d + g) S + eta S_eta + u_d |y| + eta,
@@ -445,4 +463,7 @@ def residue_elementwise_bound(rb, x, w, dtype, yref, pad=1, mma_rel=0.0, safety=
     S = _scatter_tiles(sep2(absAPT, Z.reshape(D, D, K, Tn)), N, K, th, tw, m, Ho, Wo)
     S_eta = _scatter_tiles(sep2(absAPT, Ze.reshape(D, D, K, Tn)), N, K, th, tw, m, Ho, Wo)
     g = (8 + 2 * nx + 2 + 4 + C * int(per_point.max()) + 2 * D + 2) * u32 + mma_rel
-    return safety * ((2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta)
+    b = (2 * u_d + g) * S + eta * S_eta + u_d * np.abs(yref) + eta
+    if m_store == "dtype":   # reading M3: the domain sum rounded once (see elementwise_bound)
+        b = b + u_d * S + eta * absAPT.sum(axis=1).max() ** 2
+    return safety * b

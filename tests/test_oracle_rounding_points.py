@@ -216,3 +216,55 @@ def test_pairwise_sum_tree_shape():
     assert P.pairwise_sum(list("abcdef"), add) == "(((a+b)+(c+d))+(e+f))"
     assert P.pairwise_sum(list("abcdefg"), add) == "(((a+b)+(c+d))+((e+f)+g))"
     assert P.pairwise_sum(list("a"), add) == "a"
+
+
+# --------------------------------------------------------------------------- M storage (reading M3)
+
+
+@pytest.mark.parametrize("case", _gold()["pipeline_M_dtype"]["cases"], ids=lambda c: c["dtype"])
+def test_pipeline_m_store_dtype_rounds_M_once(case):
+    """m_store="dtype": the fp32 channel sum M is rounded once to the dtype
+    before the output transform.  The golden file states M (exact), its ties
+    and both models' y; here M is recomputed with Fractions from the literal
+    lin2 matrices, the stated ties are checked against a torch cast, and the
+    oracle must give y_fp32_M with m_store="fp32" and y_dtype_M with "dtype"."""
+    G, BT, AT = _lin2()
+    dt, big = case["dtype"], case["big"]
+    d = [[[Fr(0)] * 4 for _ in range(4)] for _ in range(2)]
+    g = [[[Fr(0)] * 3 for _ in range(3)] for _ in range(2)]
+    d[0][1][1], g[0][1][1] = Fr(big), Fr(1)
+    (a, b), (i1, j1) = case["pos1"], case["tap1"]
+    d[1][a][b], g[1][i1][j1] = Fr(1), Fr(1)
+    M = [[sum(sum(G[p][i] * g[c][i][j] * G[q][j] for i in range(3) for j in range(3)) *
+              sum(BT[p][i] * d[c][i][j] * BT[q][j] for i in range(4) for j in range(4)) for c in range(2))
+          for q in range(4)] for p in range(4)]
+    assert [[str(v) for v in r] for r in M] == case["M_exact"]
+    rM = [[Fr(_cast(v, dt)) for v in r] for r in M]
+    changed = {str(M[p][q]): str(rM[p][q]) for p in range(4) for q in range(4) if rM[p][q] != M[p][q]}
+    assert changed == case["ties"]
+    y_hand = [[_cast(sum(AT[i][p] * rM[p][q] * AT[j][q] for p in range(4) for q in range(4)), dt)
+               for j in range(2)] for i in range(2)]
+    assert y_hand == case["y_dtype_M"] and y_hand != case["y_fp32_M"]
+    mods, m = T.canonical("lin2")
+    ts = T.make_transforms(mods, m)
+    x = np.zeros((1, 2, 4, 4), np.float32)
+    w = np.zeros((1, 2, 3, 3), np.float32)
+    x[0, 0, 1, 1], w[0, 0, 1, 1] = big, 1.0
+    x[0, 1, a, b], w[0, 1, i1, j1] = 1.0, 1.0
+    assert P.pipeline_conv2d(ts, x, w, dt, pad=0)[0, 0].tolist() == case["y_fp32_M"]
+    assert P.pipeline_conv2d(ts, x, w, dt, pad=0, m_store="dtype")[0, 0].tolist() == case["y_dtype_M"]
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_m_store_dtype_bound_holds(dtype):
+    """The M3 elementwise bound covers the dtype-M oracle on a random layer, and
+    the plain R1 bound does not need to (the extra u_d S term is what M adds)."""
+    from oracle import conv as CV
+    import datagen
+    mods, m = T.canonical("lin4")
+    ts = T.make_transforms(mods, m)
+    x, w = datagen.layer(1, 16, 8, 12, 12, dtype, seed=3)
+    yref = CV.direct_conv2d_f64(x, w, pad=1)
+    y = P.pipeline_conv2d(ts, x, w, dtype, m_store="dtype")
+    bd = P.elementwise_bound(ts, x, w, dtype, yref, m_store="dtype")
+    assert np.all(np.abs(y - yref) <= bd)
