@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
                     help="strong: the workload's global batch is split over the ranks; weak: every rank runs it")
     ap.add_argument("--graph", default="on", choices=["on", "off"], help="time the step as one CUDA graph")
+    ap.add_argument("--m-store", default="fp32", choices=["fp32", "dtype"],
+                    help="M between K3 and K4: fp32 (reading R1) or rounded once to the layer dtype (reading M3)")
     return ap.parse_args()
 
 
@@ -267,6 +269,8 @@ def main():
     c = WORKLOADS[a.workload]
     spec, m = canonical_spec(a.algo)
     algo = Wn.WinoAlgo(spec, m, lowering=a.lowering)
+    if a.m_store == "dtype":
+        algo.set_m_storage("dtype")
     tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[a.dtype]
     N = c["N"]                                      # the workload's (global) batch
     lo, hi = rank_batch(N, world, rank, a.scaling)
@@ -341,7 +345,8 @@ def main():
            "warmup": max(3, a.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
            "vs_baseline": None, "dtype": a.dtype, "data": "synthetic",
            "config": {"workload": c["desc"], "algo": f"{a.algo} {{{spec}}} m={m} mu={algo.mu} ratio={algo.ratio_2d:.4g}",
-                      "lowering": a.lowering, "layout": a.layout, "global_batch": n_job, "per_gpu_batch": nl,
+                      "lowering": a.lowering, "layout": a.layout, "m_store": a.m_store,
+                      "global_batch": n_job, "per_gpu_batch": nl,
                       "parallelism": f"dp{world} (batch-partitioned, no data-path collective)",
                       "launch": "CUDA graph per step" if graph is not None else "eager",
                       "l2": "inputs larger than L2 (x %.0f MB per GPU; V and M staged through HBM)" % (
@@ -359,13 +364,13 @@ def main():
 
 
 def layer_bytes(nl, C, K, H, W, es, g):
-    """Compulsory (x + w + y) and staged (+ U, V and the fp32 M written and read)
-    bytes of one layer on one GPU."""
+    """Compulsory (x + w + y) and staged (+ U, V and M written and read) bytes of
+    one layer on one GPU; M is fp32 (R1) or 16-bit (M3)."""
     pl = g["planes"]
     xb, yb, wb = nl * C * H * W * es, nl * K * H * W * es, K * C * 9 * es
     Ub = pl * g["S"] * K * g["Cp"] * es
     Vb = pl * g["Q"] * g["T"] * g["Cp"] * es
-    Mb = g["Q"] * K * g["T"] * 4
+    Mb = g["Q"] * K * g["T"] * g.get("mes", 4)
     return dict(x=xb, y=yb, w=wb, U=Ub, V=Vb, M=Mb, compulsory=xb + yb + wb, staged=xb + yb + wb + Ub + 2 * Vb + 2 * Mb)
 
 
@@ -462,6 +467,13 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
         for dt in ("bf16", "fp16", "fp32"):
             if dt != a.dtype:
                 out["rooflines_by_dtype"][dt] = dtype_roofline(a, algo, dt, c, st, peaks, peak_src)
+        # the same layer with M stored in the 16-bit dtype (reading M3), bf16 and fp16
+        if a.m_store == "fp32":
+            from paper_1905_05233_b200.algos import canonical_spec as _cs
+            sp_, m_ = _cs(a.algo)
+            a16 = Wn.WinoAlgo(sp_, m_, lowering=a.lowering).set_m_storage("dtype")
+            out["m_store_dtype"] = {dt: dtype_roofline(a, a16, dt, c, st, peaks, peak_src, accuracy=True)
+                                    for dt in ("bf16", "fp16")}
     # ---------------------------------------------------------------- end to end (host buffers)
     out["e2e"] = e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist)
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1 only)
@@ -471,9 +483,10 @@ def extras(a, out, algo, x, w, y, ws, st, nl, C, K, H, W, m, world, rank, dist, 
         out["sweep"] = sweep(c, st, peaks)
 
 
-def dtype_roofline(a, algo, dt, c, st, peaks, peak_src):
+def dtype_roofline(a, algo, dt, c, st, peaks, peak_src, accuracy=False):
     """Step time, dominant-kernel roofline and layer fractions of the workload in
-    another dtype (same algorithm)."""
+    another dtype (same algorithm); accuracy=True adds the error statistics
+    against the fp64 direct convolution (device)."""
     import numpy as np
     import torch
     import datagen
@@ -497,12 +510,22 @@ def dtype_roofline(a, algo, dt, c, st, peaks, peak_src):
         e1.record(st)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
+    acc = None
+    if accuracy:
+        yref = Wn.wino_direct_conv2d_f64(x, w, 1, stream=st)
+        s8 = Wn.wino_error_stats(y, yref, algo.m, stream=st).cpu()
+        acc = {k: (float(v) if not isinstance(v, int) else v) for k, v in Wn.summary(s8).items()}
+        del yref
     kernels, roof, B, gemm_flops = kernel_rooflines(algo, dt, x, w, y, ws, st, N, C, K, H, W, 20, 0, peaks,
                                                     peak_src, a)
     del x, w, y, ws
     torch.cuda.empty_cache()
-    return {"ms_per_step": ms, "value": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12, "kernels": kernels,
-            "roofline": roof, "layer_roofline": layer_fracs(ms, B, gemm_flops, dt, peaks)}
+    r = {"ms_per_step": ms, "value": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12, "kernels": kernels,
+         "roofline": roof, "layer_roofline": layer_fracs(ms, B, gemm_flops, dt, peaks)}
+    if acc is not None:
+        r["accuracy"] = acc
+        r["m_store"] = getattr(algo, "m_store", "fp32")
+    return r
 
 
 def per_kernel_times(algo, x, w, y, ws, st, nl, C, K, H, W, dt, reps, lay=0):

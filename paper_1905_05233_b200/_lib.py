@@ -41,6 +41,7 @@ _SIGS = {
     "wino_algo_matrix": (_I, [_P, ctypes.c_char, _P, _P, _P]),
     "wino_algo_units": (_I, [_P, _P, _P, _P, _P, _P]),
     "wino_scale_transforms": (_I, [_P, ctypes.c_int32]),
+    "wino_set_m_storage": (_I, [_P, ctypes.c_int32]),
     "wino_last_error": (ctypes.c_char_p, []),
     "wino_algo_destroy": (None, [_P]),
     "wino_conv2d_workspace": (_I, [_P, _I, _I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(ctypes.c_size_t)]),

@@ -84,6 +84,7 @@ class WinoAlgo:
         self._h = h
         self.spec = moduli if isinstance(moduli, str) else None
         self.lowering = lowering
+        self.m_store = "fp32"
         vals = [ctypes.c_int32() for _ in range(5)]
         ratio = ctypes.c_double()
         check(lib().wino_algo_info(h, *[ctypes.byref(v) for v in vals], ctypes.byref(ratio)))
@@ -107,6 +108,15 @@ class WinoAlgo:
     def scale(self, mode="pow2"):
         """Power-of-two point balancing (wino_scale_transforms, [Vincent17] per P:607)."""
         check(lib().wino_scale_transforms(self._h, {"none": 0, "pow2": 1}[mode]))
+        return self
+
+    def set_m_storage(self, mode="dtype"):
+        """Where the channel sum M lives between K3 and K4 (wino_set_m_storage):
+        "fp32" (reading R1, default) or "dtype" (reading M3: the fp32
+        accumulator rounded once to the layer's 16-bit dtype; fp32 layers and
+        tiles beyond 8x8 keep fp32)."""
+        check(lib().wino_set_m_storage(self._h, {"fp32": 0, "dtype": 1}[mode]))
+        self.m_store = mode
         return self
 
     def unit_table(self):
@@ -217,8 +227,10 @@ def geometry(algo, N, C, H, W, K, pad=1, dtype="bf16"):
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
     th, tw = -(-Ho // m), -(-Wo // m)
     T = N * th * tw
+    m16 = getattr(algo, "m_store", "fp32") == "dtype" and dtype != "fp32" and algo.m <= 8
     return dict(Ho=Ho, Wo=Wo, th=th, tw=tw, T=T, Tp=-(-T // 32) * 32, Cp=-(-C // 64) * 64, Q=D * D, S=S,
-                planes=2 if dtype == "fp32" else 1, TB=-(-T // 128), CBW=32 if dtype == "fp32" else 64)
+                planes=2 if dtype == "fp32" else 1, TB=-(-T // 128), CBW=32 if dtype == "fp32" else 64,
+                mes=2 if m16 else 4)
 
 
 def v_to_dense(V, T):
@@ -268,16 +280,21 @@ def wino_input_transform(x, algo, pad=1, stream=None, layout="nchw"):
 
 
 def wino_domain_gemm(V, U, algo, C, K, T, stream=None):
-    """M [Q][K][Tp] fp32 from blocked V (T tiles) and U."""
+    """M [Q][K][Tp] from blocked V (T tiles) and U: fp32, or V's 16-bit dtype when
+    the algorithm stores M in the dtype (set_m_storage, reading M3)."""
     dt = _TORCH_DT[V.dtype]
     Tp = -(-T // 32) * 32
-    M = torch.empty((algo.domain ** 2, K, Tp), dtype=torch.float32, device=V.device)
+    mdt = V.dtype if (algo.m_store == "dtype" and dt != "fp32" and algo.m <= 8) else torch.float32
+    M = torch.empty((algo.domain ** 2, K, Tp), dtype=mdt, device=V.device)
     with torch.cuda.device(V.device):
         check(lib().wino_domain_gemm(_ptr(V), _ptr(U), T, C, K, algo.handle, DTYPES[dt], _ptr(M), _stream(stream, V.device)))
     return M
 
 
 def wino_output_transform(M, algo, N, K, H, W, pad=1, dtype="bf16", stream=None, layout="nchw"):
+    want = TORCH_OF[dtype] if (algo.m_store == "dtype" and dtype != "fp32" and algo.m <= 8) else torch.float32
+    if M.dtype != want:
+        raise WinoError(1, f"M must be {want} for this algorithm's M storage ({algo.m_store}); got {M.dtype}")
     Ho, Wo = H + 2 * pad - 2, W + 2 * pad - 2
     shape = (N, K, Ho, Wo) if layout == "nchw" else (N, Ho, Wo, K)
     y = torch.empty(shape, dtype=TORCH_OF[dtype], device=M.device)

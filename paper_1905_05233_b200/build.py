@@ -15,8 +15,13 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build_obj")
 LIB = os.path.join(HERE, "libwino.so")
-SOURCES = ["capi_host.cpp", "generator.cpp", "transforms.cu", "xform_f32.cu", "xform_f16.cu", "xform_bf16.cu",
-           "gemm.cu", "split.cu", "conv.cu", "misc.cu"]
+# (source, object name, extra defines): xform.cu is compiled once per dtype x kind
+# (input / output transform) x m-range slice, so its large instantiations build in parallel
+XFORM = [("xform.cu", f"xform_{k}_{d}_{p}.cu", [f"-DWINO_XF_DT={d}", f"-DWINO_XF_KIND={k}", f"-DWINO_XF_PART={p}"])
+         for k in (0, 1) for d in (0, 1, 2) for p in (0, 1, 2)]
+UNITS = XFORM + [(s, s, []) for s in ["capi_host.cpp", "generator.cpp", "transforms.cu", "gemm.cu", "split.cu",
+                                      "conv.cu", "misc.cu"]]
+SOURCES = sorted({u[0] for u in UNITS})
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -60,22 +65,23 @@ def _deps(src):
 def build(force=False, jobs=None, verbose=False):
     os.makedirs(OBJ, exist_ok=True)
     objs, todo = [], []
-    for s in SOURCES:
-        o = os.path.join(OBJ, s + ".o")
+    # the largest units first (they bound the wall time)
+    for s, name, defs in sorted(UNITS, key=lambda u: (u[0] != "xform.cu", u[2][1:] if u[2] else [])):
+        o = os.path.join(OBJ, name + ".o")
         objs.append(o)
         dep_mtime = max(os.path.getmtime(p) for p in _deps(s))
         if force or not os.path.exists(o) or os.path.getmtime(o) < dep_mtime:
-            todo.append((s, o))
+            todo.append((s, o, defs))
 
     def compile_one(item):
-        s, o = item
-        cmd = [nvcc()] + _flags(s) + ["-c", os.path.join(CSRC, s), "-o", o]
+        s, o, defs = item
+        cmd = [nvcc()] + _flags(s) + defs + ["-c", os.path.join(CSRC, s), "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"compile failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         if verbose and (r.stdout or r.stderr):
             print(r.stdout + r.stderr)
-        return s
+        return os.path.basename(o)
 
     if todo:
         with ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 1)) as ex:

@@ -53,6 +53,7 @@ struct wino_algo {
   int m = 0, r = 3, nx = 0, mu = 0, D = 0, units = 0;
   wino_lowering lowering = WINO_LOWER_SUBSOLVER;
   bool scaled = false;   // wino_scale_transforms applied
+  int m_store = 0;       // wino_set_m_storage: 0 = fp32 M (reading R1), 1 = M in the 16-bit layer dtype (M3)
   std::vector<wino::Modulus> mods;
   wino::Mat G, B, A;  // exact, selected lowering: G D x r, B nx x D, A D x m
   std::vector<int> out_pt, in_pt, nterm, ta;

@@ -232,4 +232,11 @@ wino_status wino_scale_transforms(wino_algo* al, int32_t mode) {
   return WINO_OK;
 }
 
+wino_status wino_set_m_storage(wino_algo* al, int32_t mode) {
+  if (!al) return set_last_error("wino_set_m_storage: NULL algo"), WINO_E_ARG;
+  if (mode != WINO_M_FP32 && mode != WINO_M_DTYPE) return set_last_error("wino_set_m_storage: bad mode"), WINO_E_ARG;
+  al->m_store = mode;
+  return WINO_OK;
+}
+
 }  // extern "C"

@@ -13,10 +13,10 @@ wino_status run_weight_transform(const void* w, int K, int C, const wino_algo* a
 wino_status run_input_transform(const void* x, int N, int C, int H, int W, int pad, const wino_algo* al,
                                 wino_dtype dt, wino_layout layout, void* V, cudaStream_t st);
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
-                            float* M, cudaStream_t st, int mb0 = 0, int nT = -1);
+                            void* M, cudaStream_t st, int mb0 = 0, int nT = -1);
 wino_status run_domain_gemm_split(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
                                   float* M, void* y, int* cnt, cudaStream_t st);
-wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
+wino_status run_output_transform(const void* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
                                  wino_dtype dt, wino_layout layout, void* y, cudaStream_t st, int t0 = 0,
                                  int nT = -1, int Tpm = 0, int disc = 0);
 }  // namespace wino
@@ -99,11 +99,12 @@ wino_status wino_conv2d(const void* x, const void* w, int N, int C, int H, int W
   WINO_CUDA_CHECK(cudaEventRecord(ev_join, s_w));
   if ((s = run_input_transform(x, N, C, H, W, pad, al, dt, layout, V, st)) != WINO_OK) return s;
   WINO_CUDA_CHECK(cudaStreamWaitEvent(st, ev_join, 0));
-  if (layout == WINO_NCHW && !fused_disabled()) {
+  const bool m16 = m_in_dtype(al, dt);   // M3: the opt-in fused / chunked paths keep an fp32 M
+  if (layout == WINO_NCHW && !fused_disabled() && !m16) {
     s = run_domain_gemm_split(V, U, g, al, dt, M, out, reinterpret_cast<int*>(base + g.offD), st);
     if (s != WINO_E_UNSUPPORTED) return s;   // OK or a real failure
   }
-  const int cb = chunk_blocks(g, layout);
+  const int cb = m16 ? 0 : chunk_blocks(g, layout);
   if (cb > 0 && cb < g.TB) {
     // K3 -> K4 per slice of cb tile blocks through one L2-sized M slice that K4
     // discards after reading: M never travels to HBM (see chunk_blocks)
@@ -218,7 +219,7 @@ wino_status wino_input_transform(const void* x, int N, int C, int H, int W, int 
 }
 
 wino_status wino_domain_gemm(const void* V, const void* U, int T, int C, int K, const wino_algo* al,
-                             wino_dtype dt, float* M, void* stream) {
+                             wino_dtype dt, void* M, void* stream) {
   reset_launch_count();
   if (!al || !V || !U || !M || T <= 0 || C <= 0 || K <= 0) return set_last_error("bad argument"), WINO_E_ARG;
   if (reinterpret_cast<uintptr_t>(V) % 16 || reinterpret_cast<uintptr_t>(U) % 16)
@@ -230,7 +231,7 @@ wino_status wino_domain_gemm(const void* V, const void* U, int T, int C, int K, 
   return run_domain_gemm(V, U, g, al, dt, M, reinterpret_cast<cudaStream_t>(stream));
 }
 
-wino_status wino_output_transform(const float* M, int N, int K, int H, int W, int pad, const wino_algo* al,
+wino_status wino_output_transform(const void* M, int N, int K, int H, int W, int pad, const wino_algo* al,
                                   wino_dtype dt, wino_layout layout, void* out, void* stream) {
   reset_launch_count();
   wino_status s = check_layer(al, N, 1, H, W, K, pad, dt, layout);

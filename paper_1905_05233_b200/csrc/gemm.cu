@@ -35,7 +35,16 @@
 
 namespace wino {
 
-template <bool kTF32, int BN, int STAGES>
+// M element of the epilogue store: 0 = fp32 (reading R1), 1 = fp16, 2 = bf16
+// (reading M3: the fp32 accumulator rounded once to the layer dtype, RNE)
+template <int MT>
+__device__ __forceinline__ void epi_put(float* buf, int idx, float v) {
+  if constexpr (MT == 0) buf[idx] = v;
+  else if constexpr (MT == 1) reinterpret_cast<__half*>(buf)[idx] = __float2half_rn(v);
+  else reinterpret_cast<__nv_bfloat16*>(buf)[idx] = __float2bfloat16_rn(v);
+}
+
+template <bool kTF32, int BN, int STAGES, int MT = 0>
 __global__ void __launch_bounds__(256, 1)
     domain_gemm_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                        const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB, int nNB, int Q, int S,
@@ -158,7 +167,7 @@ __global__ void __launch_bounds__(256, 1)
         if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();   // the store that last read `buf` is done
         named_bar_sync(1, 128);
 #pragma unroll
-        for (int jj = 0; jj < 32; ++jj) buf[jj * kBM + wq * 32 + lane] = v[jj];
+        for (int jj = 0; jj < 32; ++jj) epi_put<MT>(buf, jj * kBM + wq * 32 + lane, v[jj]);
         fence_proxy_async_shared();
         named_bar_sync(1, 128);
         if (storer) {
@@ -223,7 +232,7 @@ __device__ __forceinline__ void tma_store_3d_hint(const CUtensorMap* map, const 
       : "memory");
 }
 
-template <bool kTF32, int STAGES, int EPI, bool kHint, int EC>
+template <bool kTF32, int STAGES, int EPI, bool kHint, int EC, int MT = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     domain_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
                             const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB2, int nNB, int Q,
@@ -366,7 +375,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
           if (storer) bulk_wait_read<Cfg::EPI_BUFS - 1>();
           named_bar_sync(1, 128);
 #pragma unroll
-          for (int jj = 0; jj < EC; ++jj) buf[jj * kBM + wq * 32 + lane] = v[h + jj];
+          for (int jj = 0; jj < EC; ++jj) epi_put<MT>(buf, jj * kBM + wq * 32 + lane, v[h + jj]);
           fence_proxy_async_shared();
           named_bar_sync(1, 128);
           if (storer) {
@@ -391,11 +400,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <bool kTF32, int STAGES, int EPI, bool kHint, int EC = 32>
+template <bool kTF32, int STAGES, int EPI, bool kHint, int EC = 32, int MT = 0>
 static wino_status launch_gemm_pair(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
                                     const GemmSched& gs, uint32_t fmt, int mb0, int nT, cudaStream_t st) {
   using Cfg = PairCfg<kTF32, STAGES, EPI, EC>;
-  auto kern = domain_gemm_pair_kernel<kTF32, STAGES, EPI, kHint, EC>;
+  auto kern = domain_gemm_pair_kernel<kTF32, STAGES, EPI, kHint, EC, MT>;
   WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const int nMB2 = (nT + 2 * kBM - 1) / (2 * kBM), nNB = (g.K + Cfg::BN - 1) / Cfg::BN;
   const int items = g.Q * nMB2 * nNB;
@@ -421,11 +430,11 @@ static wino_status launch_gemm_pair(const CUtensorMap& tv, const CUtensorMap& tu
   return WINO_OK;
 }
 
-template <bool kTF32, int BN, int STAGES>
+template <bool kTF32, int BN, int STAGES, int MT = 0>
 static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm, const Geo& g,
                                const GemmSched& gs, uint32_t fmt, int mb0, int nT, cudaStream_t st) {
   using Cfg = GemmCfg<kTF32, BN, STAGES>;
-  auto kern = domain_gemm_kernel<kTF32, BN, STAGES>;
+  auto kern = domain_gemm_kernel<kTF32, BN, STAGES, MT>;
   // (a per-device attribute: set on every launch, it is a cheap host call)
   WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   const int nMB = (nT + kBM - 1) / kBM, nNB = (g.K + BN - 1) / BN;
@@ -445,21 +454,45 @@ static bool pair_enabled() {
 }
 
 // M_xi for the tiles [mb0 * 128, mb0 * 128 + nT) of V (all of them by default) into
-// M [Q][K][Tpm] with Tpm = nT rounded up to 32 (chunked layers: an L2-sized slice)
+// M [Q][K][Tpm] with Tpm = nT rounded up to 32 (chunked layers: an L2-sized slice);
+// M is fp32, or the layer dtype for 16-bit layers when the algorithm stores M in
+// the dtype (wino_set_m_storage, reading M3)
+template <int MT>
+static wino_status launch_domain_gemm_16(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm,
+                                         const void* U, const Geo& g, const wino_algo* al, CUtensorMapDataType cdt,
+                                         uint32_t fmt, int BN, int mb0, int nT, cudaStream_t st) {
+  const uint32_t BK = 128 / (uint32_t)g.es;
+  if (BN == 256 && nT > kBM && pair_enabled()) {
+    CUtensorMap tu2;   // B boxes of 128 k rows: each CTA of the pair loads half of the 256-wide tile
+    if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {
+      set_last_error("cuTensorMapEncodeTiled failed");
+      return WINO_E_CUDA;
+    }
+    // 6 stages + 2 epilogue buffers: 237 us on cfg5 lin4 bf16 (5 + 4: 248; 4 + 6: 262;
+    // 3 + 8: 296; 16-column store boxes or an evict-first L2 hint on the M stores: +-2)
+    return launch_gemm_pair<false, 6, 2, false, 32, MT>(tv, tu2, tm, g, al->gs, fmt, mb0, nT, st);
+  }
+  if (BN == 256) return launch_gemm<false, 256, 4, MT>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);   // 3 stages + 4 epilogue buffers: 8 % slower
+  if (BN == 128) return launch_gemm<false, 128, 6, MT>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+  return launch_gemm<false, 64, 8, MT>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+}
+
 wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wino_algo* al, wino_dtype dt,
-                            float* M, cudaStream_t st, int mb0, int nT) {
+                            void* M, cudaStream_t st, int mb0, int nT) {
   if (nT < 0) nT = g.T;
   const int Tpm = (nT + 31) / 32 * 32;
   const bool tf32 = dt == WINO_F32;
   CUtensorMapDataType cdt = dt == WINO_F32   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                             : dt == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const bool m16 = m_in_dtype(al, dt);
   int BN = tf32 ? (g.K > 64 ? 128 : 64) : (g.K > 128 ? 256 : (g.K > 64 ? 128 : 64));
   const uint32_t BK = 128 / (uint32_t)g.es;
   CUtensorMap tv, tu, tm;
   if (!make_map3(&tv, cdt, g.es, V, BK, kBM, (uint64_t)g.planes * g.Q * g.TB * (g.Cp / BK), BK, kBM) ||
       !make_map3(&tu, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, BN) ||
-      !make_map3(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, nT, g.K, g.Q, kBM, 32, false, Tpm)) {
+      !make_map3(&tm, m16 ? cdt : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, m16 ? 2 : 4, M, nT, g.K, g.Q, kBM, 32, false,
+                 Tpm)) {
     set_last_error("cuTensorMapEncodeTiled failed (driver entry point unavailable or bad geometry)");
     return WINO_E_CUDA;
   }
@@ -477,19 +510,9 @@ wino_status run_domain_gemm(const void* V, const void* U, const Geo& g, const wi
     if (BN == 128) return launch_gemm<true, 128, 3>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
     return launch_gemm<true, 64, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
   }
-  if (BN == 256 && nT > kBM && pair_enabled()) {
-    CUtensorMap tu2;   // B boxes of 128 k rows: each CTA of the pair loads half of the 256-wide tile
-    if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {
-      set_last_error("cuTensorMapEncodeTiled failed");
-      return WINO_E_CUDA;
-    }
-    // 6 stages + 2 epilogue buffers: 237 us on cfg5 lin4 bf16 (5 + 4: 248; 4 + 6: 262;
-    // 3 + 8: 296; 16-column store boxes or an evict-first L2 hint on the M stores: +-2)
-    return launch_gemm_pair<false, 6, 2, false>(tv, tu2, tm, g, al->gs, fmt, mb0, nT, st);
-  }
-  if (BN == 256) return launch_gemm<false, 256, 4>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);   // 3 stages + 4 epilogue buffers: 8 % slower
-  if (BN == 128) return launch_gemm<false, 128, 6>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
-  return launch_gemm<false, 64, 8>(tv, tu, tm, g, al->gs, fmt, mb0, nT, st);
+  if (!m16) return launch_domain_gemm_16<0>(tv, tu, tm, U, g, al, cdt, fmt, BN, mb0, nT, st);
+  if (dt == WINO_F16) return launch_domain_gemm_16<1>(tv, tu, tm, U, g, al, cdt, fmt, BN, mb0, nT, st);
+  return launch_domain_gemm_16<2>(tv, tu, tm, U, g, al, cdt, fmt, BN, mb0, nT, st);
 }
 
 }  // namespace wino

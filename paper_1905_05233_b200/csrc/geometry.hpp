@@ -1,5 +1,6 @@
 // geometry.hpp -- layer geometry and workspace layout of wino_conv2d
-// (include/wino.h): U [S][K][Cp] | V [TB][Cp/CBW][Q][128][CBW] | M [Q][K][Tp] fp32 | group counters.
+// (include/wino.h): U [S][K][Cp] | V [TB][Cp/CBW][Q][128][CBW] | M [Q][K][Tp] (fp32, or the
+// 16-bit dtype under wino_set_m_storage) | group counters.
 #pragma once
 #include <cstddef>
 
@@ -9,12 +10,19 @@ namespace wino {
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// M between K3 and K4 in the layer's 16-bit dtype (reading M3)?  fp32 layers keep fp32, and so
+// do tiles beyond 8x8 (their output transforms weigh M by entries up to ~1e4, SURVEY H1 option 5).
+inline bool m_in_dtype(const wino_algo* al, wino_dtype dt) {
+  return al->m_store == 1 && dt != WINO_F32 && al->m <= 8;
+}
+
 struct Geo {
   int N, C, H, W, K, pad;
   int m, D, Q, S;
   int Ho, Wo, th, tw, T, Tp, Cp;
   int TB, CBW;   // V blocks: 128 tiles x CBW channels (one 128-byte swizzle row per tile)
   size_t es, planes;
+  size_t mes;    // bytes per M element: 4 (fp32, R1) or 2 (the 16-bit layer dtype, M3)
   size_t offU, offV, offM, offD, total;
 };
 
@@ -50,7 +58,8 @@ inline Geo make_geo(const wino_algo* al, int N, int C, int H, int W, int K, int 
   g.CBW = (int)(128 / g.es);
   size_t v_bytes = g.planes * (size_t)g.Q * g.TB * 128 * g.Cp * g.es;
   // M: [Q][K][Tp] for the staged K3 -> K4 pair, [TB][K][Q][128] for the fused split kernel
-  size_t m_bytes = (size_t)g.Q * K * g.TB * 128 * 4;
+  g.mes = m_in_dtype(al, dt) ? 2 : 4;
+  size_t m_bytes = (size_t)g.Q * K * g.TB * 128 * g.mes;
   g.offU = 0;
   g.offV = align_up(g.offU + u_bytes, 1024);
   g.offM = align_up(g.offV + v_bytes, 1024);

@@ -11,14 +11,23 @@
 
 namespace wino {
 
+// table slices of xform.cu: kXf<kind>_<dtype>_<part>, part 0: m = 2..5, 1: 6..8, 2: 9..12
+#define XF_DECL(k, d)                                     \
+  extern const XfT##k kXf##k##_##d##_0[kXfRows0][kTabD]; \
+  extern const XfT##k kXf##k##_##d##_1[kXfRows1][kTabD]; \
+  extern const XfT##k kXf##k##_##d##_2[kXfRows2][kTabD];
+using XfT0 = InFn;
+using XfT1 = OutFn;
+XF_DECL(0, 0) XF_DECL(0, 1) XF_DECL(0, 2) XF_DECL(1, 0) XF_DECL(1, 1) XF_DECL(1, 2)
+#undef XF_DECL
+#define XF_PICK(k, d) (m <= 5 ? kXf##k##_##d##_0[m - 2][doff] : m <= 8 ? kXf##k##_##d##_1[m - 6][doff] : kXf##k##_##d##_2[m - 9][doff])
 static InFn in_fn_(int dt, int m, int doff) {
-  const InFn(*t)[kTabD] = dt == WINO_F32 ? kInTableF32 : dt == WINO_F16 ? kInTableF16 : kInTableBF16;
-  return t[m - 2][doff];
+  return dt == WINO_F32 ? XF_PICK(0, 0) : dt == WINO_F16 ? XF_PICK(0, 1) : XF_PICK(0, 2);
 }
 static OutFn out_fn_(int dt, int m, int doff) {
-  const OutFn(*t)[kTabD] = dt == WINO_F32 ? kOutTableF32 : dt == WINO_F16 ? kOutTableF16 : kOutTableBF16;
-  return t[m - 2][doff];
+  return dt == WINO_F32 ? XF_PICK(1, 0) : dt == WINO_F16 ? XF_PICK(1, 1) : XF_PICK(1, 2);
 }
+#undef XF_PICK
 
 // (m, D) with compiled transform kernels (WINO_TABLE)
 static bool md_ok(const wino_algo* al) {
@@ -101,7 +110,7 @@ wino_status run_input_transform(const void* x, int N, int C, int H, int W, int p
   return WINO_OK;
 }
 
-wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
+wino_status run_output_transform(const void* Mw, int N, int K, int H, int W, int pad, const wino_algo* al,
                                  wino_dtype dt, wino_layout layout, void* y, cudaStream_t st, int t0, int nT,
                                  int Tpm, int disc) {
   if ((layout != WINO_NCHW && layout != WINO_NHWC) || !md_ok(al)) {
@@ -111,6 +120,7 @@ wino_status run_output_transform(const float* Mw, int N, int K, int H, int W, in
   Geo g = make_geo(al, N, 1, H, W, K, pad, dt);
   OutArgs a{Mw, K, g.Ho, g.Wo, g.th, g.tw, g.T, nT < 0 ? g.Tp : Tpm, (int)layout, &al->xp, y, st};
   a.t0 = t0, a.nT = nT, a.disc = disc;
+  a.m16 = m_in_dtype(al, dt) ? 1 : 0;
   out_fn_(dt, al->m, al->D - al->m - 2)(a);
   WINO_LAUNCH_CHECK();
   return WINO_OK;

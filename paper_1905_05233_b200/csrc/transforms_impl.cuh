@@ -377,15 +377,27 @@ __device__ __forceinline__ void transform_tile_pairs(const float2* ring, int s0,
 //   mode 1 (3D):   box {BOXC, RB, 64} of the [N*C][H][W] view (W*es % 16 == 0)
 // TMA zero-fills rows / columns outside the image.
 template <int DT> struct PairT;
+// pack2(ra, rb, d0, d1): columns (c, c + 1) of channels a (ra) and b (rb) -> the
+// two pairs d0 = (a_c, b_c), d1 = (a_c+1, b_c+1) with one load per channel
 template <> struct PairT<WINO_F32> {
   using T = float2;
   static __device__ __forceinline__ T pack(float a, float b) { return make_float2(a, b); }
+  static __device__ __forceinline__ void pack2(const float* ra, const float* rb, T* d0, T* d1) {
+    const float2 a = *reinterpret_cast<const float2*>(ra), b = *reinterpret_cast<const float2*>(rb);
+    *d0 = make_float2(a.x, b.x);
+    *d1 = make_float2(a.y, b.y);
+  }
   static __device__ __forceinline__ float2 unpack(T v) { return v; }
 };
 template <> struct PairT<WINO_BF16> {
   using T = uint32_t;   // (bf16 a, bf16 b): a in the low half
   static __device__ __forceinline__ T pack(__nv_bfloat16 a, __nv_bfloat16 b) {
     return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+  }
+  static __device__ __forceinline__ void pack2(const __nv_bfloat16* ra, const __nv_bfloat16* rb, T* d0, T* d1) {
+    const uint32_t a = *reinterpret_cast<const uint32_t*>(ra), b = *reinterpret_cast<const uint32_t*>(rb);
+    *d0 = __byte_perm(a, b, 0x5410);   // (a lo, b lo)
+    *d1 = __byte_perm(a, b, 0x7632);   // (a hi, b hi)
   }
   static __device__ __forceinline__ float2 unpack(T v) {
     return make_float2(__uint_as_float(v << 16), __uint_as_float(v & 0xFFFF0000u));
@@ -395,6 +407,11 @@ template <> struct PairT<WINO_F16> {
   using T = uint32_t;
   static __device__ __forceinline__ T pack(__half a, __half b) {
     return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+  }
+  static __device__ __forceinline__ void pack2(const __half* ra, const __half* rb, T* d0, T* d1) {
+    const uint32_t a = *reinterpret_cast<const uint32_t*>(ra), b = *reinterpret_cast<const uint32_t*>(rb);
+    *d0 = __byte_perm(a, b, 0x5410);   // (a lo, b lo)
+    *d1 = __byte_perm(a, b, 0x7632);   // (a hi, b hi)
   }
   static __device__ __forceinline__ float2 unpack(T v) {
     return __half22float2(*reinterpret_cast<const __half2*>(&v));
@@ -480,14 +497,28 @@ struct K1Geo {
   int mode, RB, BOXC, NSLOT, RR, SEGP;
   int ralign, calign;   // flat boxes start at a multiple of ralign rows, 3D boxes at a multiple of calign columns
   unsigned box_bytes, slot_bytes;
+  int ncb, nItems;      // column blocks; work items = ncb * N * (Cp / 64)
 };
 
+// Persistent, barrier-free pipeline: grid = min(items, 2 per SM); a CTA walks
+// work items (column block, image, 64-channel block) and, inside each, the th
+// tile rows.  Conversion step K of the CTA (item j, it = -1 .. th-1; K counts
+// across items) moves the M input rows it*M - pad + 2 .. +M-1 (n_x - m = 2
+// halo rows come from the previous step) from raw slot K % NSLOT into ring
+// group K % RG (groups of M rows, consecutive groups adjacent in the circular
+// ring of RR = RG * M rows).  Compute step (j, ti) reads groups K - 1 (its last
+// two rows) and K, K = j (th + 1) + ti + 1.  Handoffs are mbarriers only:
+//   producer warp  --raw_full (TMA tx)-->  converter warps
+//   converters     --raw_empty-->  producer;  --grp_full-->  compute warps
+//   compute warps  --grp_empty (group K - 1 after step ti; group K too after
+//                    the item's last step)-->  converters
+// so the converters run up to RG - 2 steps ahead of the math, and the next
+// item's first boxes and conversions overlap the current item's last tiles.
 template <int DT, int M, int NX, int D, typename MK = DenseBT>
-__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_small(NX, D) ? 2 : 1) input_transform_tma(const __grid_constant__ CUtensorMap tmx,
-                                                              const __grid_constant__ K1Geo gk,
-                                                              const __grid_constant__ XformParams xp,
-                                                              typename DType<DT>::T* __restrict__ V, size_t qstride,
-                                                              size_t plane) {
+__global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS + 1), k1_small(NX, D) && DT != WINO_F32 ? 2 : 1)
+    input_transform_tma(const __grid_constant__ CUtensorMap tmx, const __grid_constant__ K1Geo gk,
+                        const __grid_constant__ XformParams xp, typename DType<DT>::T* __restrict__ V,
+                        size_t qstride, size_t plane) {
   using Tr = DType<DT>;
   using TT = typename Tr::T;
   using P = PairT<DT>;
@@ -496,142 +527,182 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS), k1_sma
   // TMA destinations must be 128-byte aligned: offset the shared array (stays a
   // shared-space pointer, so accesses compile to LDS / STS)
   uint8_t* k1_smem = k1_smem_raw + ((128u - (smem_u32(k1_smem_raw) & 127u)) & 127u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(k1_smem);
-  uint8_t* raw = k1_smem + 128;
-  PT* ring = reinterpret_cast<PT*>(raw + (size_t)gk.NSLOT * gk.slot_bytes);
-  const int C = gk.C, W = gk.W, pad = gk.pad, th = gk.th, RR = gk.RR, SEGP = gk.SEGP, NSLOT = gk.NSLOT;
+  const int NSLOT = gk.NSLOT, RR = gk.RR, RG = gk.RR / M, SEGP = gk.SEGP, th = gk.th, pad = gk.pad, W = gk.W;
+  uint64_t* raw_full = reinterpret_cast<uint64_t*>(k1_smem);
+  uint64_t* raw_empty = raw_full + NSLOT;
+  uint64_t* grp_full = raw_empty + NSLOT;
+  uint64_t* grp_empty = grp_full + RG;
+  uint8_t* raw = k1_smem + 256;
+  PT* ring = reinterpret_cast<PT*>(raw + (size_t)NSLOT * gk.slot_bytes);
   const int SEG = gk.TJB * M + NX - M;
-  const int tj0 = blockIdx.x * gk.TJB;
-  const int n = blockIdx.y;
-  const int c0 = blockIdx.z * 64;
-  const int col0 = tj0 * M - pad;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const bool leader = threadIdx.x == 0;
-  const int crow = n * C + c0;   // first channel row of the box in the [N*C] dimension
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int CW = 0;                       // compute warps first
+  const int cw = (int)(blockDim.x >> 5) - K1_CONV_WARPS - 1;
+  const int conv0 = cw, prod = cw + K1_CONV_WARPS;
+  const int nCB = gk.Cp / 64;
+  (void)CW;
 
-  auto wait = [&](int it) {
-    const int s = (it + 1) % NSLOT;
-    mbar_wait(&full[s], (uint32_t)(((it + 1) / NSLOT) & 1));
-  };
-  // raw slot of step it -> packed ring rows; lanes walk ring columns b
-  // TMA boxes whose in-bounds part does not start on a 16-byte boundary of
-  // the row (negative or unaligned inner coordinates) trap as an illegal
-  // instruction (measured, scripts/tma_probe.cu), so boxes start at a
-  // non-negative, 16-byte aligned column / flat offset; the extra leading
-  // rows / columns are skipped here and rows / columns before the image are
-  // zeros.
-  const int cst = ((col0 < 0 ? 0 : col0) / gk.calign) * gk.calign;
-  // raw slot of step it -> packed ring rows (executed by the converter warps,
-  // one halo row each; lanes walk the ring columns)
-  const int cw = nw - K1_CONV_WARPS;     // compute warps
-  auto convert = [&](int it) {
-    const TT* rs = reinterpret_cast<const TT*>(raw + (size_t)((it + 1) % NSLOT) * gk.slot_bytes);
-    const int RBW = gk.mode == 0 ? gk.RB * W : gk.RB * gk.BOXC;   // elements per channel in the box
-    const int rstride = gk.mode == 0 ? W : gk.BOXC;
-    const int g0 = it * M - pad + NX - M;
-    const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
-    // ring columns [blo, bhi) are inside the image (the others stay zero)
-    const int blo = col0 < 0 ? -col0 : 0;
-    const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
-    const int qoff = gk.mode == 0 ? col0 : col0 - cst;   // raw column of ring column b: b + qoff
-    const bool allc = c0 + 64 <= C;                      // every channel of the block is real
-#pragma unroll 1
-    for (int k = warp - cw; k < M; k += nw - cw) {
-      const int g = g0 + k;
-      if (g < -pad) continue;
-      PT* drow = ring + ((g + 8 * RR) % RR) * 32 * SEGP;
-      const TT* rrow = rs + (g < 0 ? 0 : g - gst) * rstride + qoff;
-      if (g >= 0 && allc) {
-        for (int b = blo + lane; b < bhi; b += 32) {
-#pragma unroll 8
-          for (int p = 0; p < 32; ++p)
-            drow[p * SEGP + b] = P::pack(rrow[(2 * p) * RBW + b], rrow[(2 * p + 1) * RBW + b]);
-        }
-      } else {
-        for (int b = blo + lane; b < bhi; b += 32) {
-#pragma unroll 4
-          for (int p = 0; p < 32; ++p) {
-            const int ca = c0 + 2 * p;
-            const TT va = (g >= 0 && ca < C) ? rrow[(2 * p) * RBW + b] : Tr::cvt(0.f);
-            const TT vb = (g >= 0 && ca + 1 < C) ? rrow[(2 * p + 1) * RBW + b] : Tr::cvt(0.f);
-            drow[p * SEGP + b] = P::pack(va, vb);
-          }
-        }
-      }
-    }
-  };
-
-  if (leader) {
-    for (int s = 0; s < NSLOT; ++s) mbar_init(&full[s], 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSLOT; ++s) mbar_init(&raw_full[s], 1), mbar_init(&raw_empty[s], K1_CONV_WARPS * 32);
+    for (int g = 0; g < RG; ++g) mbar_init(&grp_full[g], K1_CONV_WARPS * 32), mbar_init(&grp_empty[g], cw * 32);
     fence_barrier_init();
     tma_prefetch(&tmx);
   }
-  // ring columns before the image (and, for flat boxes, after it) stay zero
-  {
-    const int blo = col0 < 0 ? -col0 : 0;
-    const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
+  __syncthreads();
+
+  // item -> (column block, image, channel block); channel blocks fastest
+  auto decode = [&](int item, int& cb, int& n, int& c0) {
+    const int cbk = item % nCB, r = item / nCB;
+    n = r % (gk.nItems / (nCB * gk.ncb));
+    cb = r / (gk.nItems / (nCB * gk.ncb));
+    c0 = cbk * 64;
+  };
+  const int nIt = gk.nItems;
+
+  if (warp == prod) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int item = blockIdx.x; item < nIt; item += gridDim.x) {
+        int cb, n, c0;
+        decode(item, cb, n, c0);
+        const int col0 = cb * gk.TJB * M - pad;
+        const int cst = ((col0 < 0 ? 0 : col0) / gk.calign) * gk.calign;
+        const int crow = n * gk.C + c0;
+        for (int it = -1; it < th; ++it) {
+          mbar_wait_sleep(&raw_empty[s], ph ^ 1);
+          const int g0 = it * M - pad + NX - M;
+          const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
+          mbar_arrive_expect_tx(&raw_full[s], gk.box_bytes);
+          if (gk.mode == 0) tma_load_2d(raw + (size_t)s * gk.slot_bytes, &tmx, &raw_full[s], gst * W, crow);
+          else tma_load_3d(raw + (size_t)s * gk.slot_bytes, &tmx, &raw_full[s], cst, gst, crow);
+          if (++s == NSLOT) s = 0, ph ^= 1;
+        }
+      }
+    }
+  } else if (warp >= conv0) {
+    // ------------------------------------------------------------ converters
+    const int cwarp = warp - conv0;
+    int s = 0, g = 0;
+    uint32_t phs = 0, phg = 0;
     const PT z = P::pack(Tr::cvt(0.f), Tr::cvt(0.f));
-    for (int r = threadIdx.x; r < RR * 32; r += blockDim.x) {
-      PT* row = ring + r * SEGP;
-      for (int b = 0; b < blo; ++b) row[b] = z;
-      for (int b = bhi; b < SEG; ++b) row[b] = z;
-    }
-  }
-  __syncthreads();
-  // TMA of the m new rows of step `it` into raw slot (it + 1) % NSLOT (leader only;
-  // written out here rather than in a lambda so the tensor map stays a kernel
-  // parameter address)
-#define K1_ISSUE(it_)                                                                                    \
-  do {                                                                                                   \
-    const int s_ = ((it_) + 1) % NSLOT;                                                                  \
-    const int g0_ = gk.mode == 0 ? (max((it_) * M - pad + NX - M, 0) / gk.ralign) * gk.ralign                \
-                                 : max((it_) * M - pad + NX - M, 0);                                   \
-    fence_proxy_async_shared();                                                                          \
-    mbar_arrive_expect_tx(&full[s_], gk.box_bytes);                                                      \
-    if (gk.mode == 0) tma_load_2d(raw + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], g0_ * W, crow);     \
-    else tma_load_3d(raw + (size_t)s_ * gk.slot_bytes, &tmx, &full[s_], cst, g0_, crow);                 \
-  } while (0)
-  // warp specialisation: warps 0 .. cw-1 transform tiles, the K1_CONV_WARPS
-  // converter warps issue the TMA boxes (lane 0 of warp cw) and converts the raw rows of step ti+1
-  // while tile row ti is transformed; one CTA barrier per step.
-  const bool conv = warp >= cw;
-  if (conv) {
-    if (warp == cw && lane == 0)
-      for (int it = -1; it < NSLOT - 1 && it < th; ++it) K1_ISSUE(it);
-    __syncwarp();
-    wait(-1);
-    convert(-1);
-    wait(0);
-    convert(0);
-  }
-  __syncthreads();
-  const int ca = c0 + 2 * lane;
+    for (int item = blockIdx.x; item < nIt; item += gridDim.x) {
+      int cb, n, c0;
+      decode(item, cb, n, c0);
+      const int col0 = cb * gk.TJB * M - pad;
+      const int cst = ((col0 < 0 ? 0 : col0) / gk.calign) * gk.calign;
+      const int RBW = gk.mode == 0 ? gk.RB * W : gk.RB * gk.BOXC;   // elements per channel in the box
+      const int rstride = gk.mode == 0 ? W : gk.BOXC;
+      // ring columns [blo, bhi) are inside the image; the others are zero
+      const int blo = col0 < 0 ? -col0 : 0;
+      const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
+      const int qoff = gk.mode == 0 ? col0 : col0 - cst;   // raw column of ring column b: b + qoff
+      const bool allc = c0 + 64 <= gk.C;                   // every channel of the block is real
+      // vector conversion: raw columns qoff + b for b in [bs, bs + 2 npair) in aligned pairs
+      // (rows and channel planes of the box start at even elements), single leading /
+      // trailing columns apart
+      const bool vec = (rstride % 2) == 0 && (RBW % 2) == 0;
+      const int bs = blo + ((qoff + blo) & 1);
+      const int npair = (bhi - bs) / 2;
+      const bool lead = bs > blo, trail = bs + 2 * npair < bhi;
+      for (int it = -1; it < th; ++it) {
+        mbar_wait_sleep(&raw_full[s], phs);
+        mbar_wait_sleep(&grp_empty[g], phg ^ 1);
+        const TT* rs = reinterpret_cast<const TT*>(raw + (size_t)s * gk.slot_bytes);
+        const int g0 = it * M - pad + NX - M;
+        const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
 #pragma unroll 1
-  for (int ti = 0; ti < th; ++ti) {
-    if (conv) {
-      if (warp == cw && lane == 0 && ti + NSLOT - 1 < th) K1_ISSUE(ti + NSLOT - 1);
-      __syncwarp();
-      if (ti + 1 < th) {
-        wait(ti + 1);
-#if !(K1_SKIP & 2)
-        convert(ti + 1);
-#endif
-      }
-    } else {
-      const int s0 = (ti * M - pad + 8 * RR) % RR;
-      for (int tjl = warp; tjl < gk.TJB; tjl += cw) {
-        const int tj = tj0 + tjl;
-        if (tj >= gk.tw) break;
-        const size_t t = ((size_t)n * th + ti) * gk.tw + tj;
-#if !(K1_SKIP & 1)
-        transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp, V + v_offset((int)t, ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
-                                           kVPointBytes / sizeof(TT), plane);
-#endif
+        for (int k = cwarp; k < M; k += K1_CONV_WARPS) {
+          const int gr = g0 + k;
+          if (gr < -pad) continue;   // never read
+          PT* drow = ring + (g * M + k) * 32 * SEGP;
+          const TT* rrow = rs + (gr < 0 ? 0 : gr - gst) * rstride + qoff;
+          for (int b = lane; b < blo; b += 32)
+#pragma unroll 4
+            for (int p = 0; p < 32; ++p) drow[p * SEGP + b] = z;
+          for (int b = bhi + lane; b < SEG; b += 32)
+#pragma unroll 4
+            for (int p = 0; p < 32; ++p) drow[p * SEGP + b] = z;
+          if (gr >= 0 && allc && vec) {
+            // two columns per lane and load (4-byte / 8-byte raw pairs): lanes 0-15 walk the
+            // column pairs, the two half-warps take the even / odd channel pairs p
+            // (odd SEGP: the half-warps store to disjoint banks)
+            const TT* r0 = rrow + bs;
+            PT* d0 = drow + bs + (lane >> 4) * SEGP;
+            for (int pi = lane & 15; pi < npair; pi += 16) {
+              const TT* src = r0 + 2 * pi + (lane >> 4) * 2 * RBW;
+              PT* dst = d0 + 2 * pi;
+#pragma unroll 4
+              for (int pp = 0; pp < 16; ++pp) {
+                P::pack2(src, src + RBW, dst, dst + 1);
+                src += 4 * RBW;
+                dst += 2 * SEGP;
+              }
+            }
+            if (lead)   // the first column alone (odd raw alignment): one channel pair per lane
+              drow[lane * SEGP + blo] = P::pack(rrow[(2 * lane) * RBW + blo], rrow[(2 * lane + 1) * RBW + blo]);
+            if (trail)
+              drow[lane * SEGP + bhi - 1] =
+                  P::pack(rrow[(2 * lane) * RBW + bhi - 1], rrow[(2 * lane + 1) * RBW + bhi - 1]);
+          } else if (gr >= 0 && allc) {
+            for (int b = blo + lane; b < bhi; b += 32) {
+#pragma unroll 8
+              for (int p = 0; p < 32; ++p)
+                drow[p * SEGP + b] = P::pack(rrow[(2 * p) * RBW + b], rrow[(2 * p + 1) * RBW + b]);
+            }
+          } else {
+            for (int b = blo + lane; b < bhi; b += 32) {
+#pragma unroll 4
+              for (int p = 0; p < 32; ++p) {
+                const int ca = c0 + 2 * p;
+                const TT va = (gr >= 0 && ca < gk.C) ? rrow[(2 * p) * RBW + b] : Tr::cvt(0.f);
+                const TT vb = (gr >= 0 && ca + 1 < gk.C) ? rrow[(2 * p + 1) * RBW + b] : Tr::cvt(0.f);
+                drow[p * SEGP + b] = P::pack(va, vb);
+              }
+            }
+          }
+        }
+        mbar_arrive(&raw_empty[s]);   // this thread is done with the raw slot
+        mbar_arrive(&grp_full[g]);    // ... and has written its ring rows
+        if (++s == NSLOT) s = 0, phs ^= 1;
+        if (++g == RG) g = 0, phg ^= 1;
       }
     }
-    __syncthreads();
+  } else {
+    // ------------------------------------------------------------ compute warps
+    int g = 0;          // group of conversion step K (the current step's new rows)
+    uint32_t phg = 0;
+    for (int item = blockIdx.x; item < nIt; item += gridDim.x) {
+      int cb, n, c0;
+      decode(item, cb, n, c0);
+      const int tj0 = cb * gk.TJB;
+      const int ca = c0 + 2 * lane;
+      // conversion (item, -1): its last two rows are the first tile row's halo
+      int gp = g;
+      mbar_wait_sleep(&grp_full[g], phg);
+      if (++g == RG) g = 0, phg ^= 1;
+#pragma unroll 1
+      for (int ti = 0; ti < th; ++ti) {
+        mbar_wait_sleep(&grp_full[g], phg);
+        const int s0 = gp * M + M - (NX - M);   // ring row of the tile's first halo row
+        const size_t t_row = ((size_t)n * th + ti) * gk.tw;
+        for (int tjl = warp; tjl < gk.TJB; tjl += cw) {
+          const int tj = tj0 + tjl;
+          if (tj >= gk.tw) break;
+#if !(K1_SKIP & 1)
+          transform_tile_ring<DT, NX, D, PT, MK>(ring + lane * SEGP, s0, RR, SEGP, tjl * M, xp,
+                                                 V + v_offset((int)(t_row + tj), ca, gk.Cp, 128 / (int)sizeof(TT), D * D),
+                                                 kVPointBytes / sizeof(TT), plane);
+#endif
+        }
+        mbar_arrive(&grp_empty[gp]);               // the older group is no longer needed
+        if (ti == th - 1) mbar_arrive(&grp_empty[g]);
+        gp = g;
+        if (++g == RG) g = 0, phg ^= 1;
+      }
+    }
   }
-#undef K1_ISSUE
 }
 
 // ------------------------------------------------------------------ K1 input transform (NHWC)
@@ -881,13 +952,20 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
 }
 
 // ------------------------------------------------------------------ K4 output transform (NCHW)
+// M element: fp32 (reading R1) or the layer's 16-bit dtype (reading M3)
+__device__ __forceinline__ float ld_m(const float* p) { return __ldg(p); }
+__device__ __forceinline__ float ld_m(const __half* p) { return __half2float(__ldg(p)); }
+__device__ __forceinline__ float ld_m(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+__device__ __forceinline__ float sm_m(const float* p) { return *p; }
+__device__ __forceinline__ float sm_m(const __half* p) { return __half2float(*p); }
+__device__ __forceinline__ float sm_m(const __nv_bfloat16* p) { return __bfloat162float(*p); }
 // One thread per (t, k), t fastest (coalesced reads of M[q][k][t]).  Row-streamed
 // separable transform: Z_i = M_{i,.} A (m values), Y += A_{i,.}^T (x) Z_i.
 // Tiles [t0, T) with M rows indexed from t0 (a chunk's M slice when t0 > 0);
 // DISC drops the consumed M lines from L2 afterwards (they are never written
 // back: chunked layers keep M in L2 only).
-template <int DT, int M, int D, bool DISC>
-__global__ void __launch_bounds__(128) output_transform_nchw(const float* __restrict__ Mw, int K, int Ho, int Wo,
+template <int DT, int M, int D, bool DISC, typename MT = float>
+__global__ void __launch_bounds__(128) output_transform_nchw(const MT* __restrict__ Mw, int K, int Ho, int Wo,
                                                              int th, int tw, int T, int Tp,
                                                              const __grid_constant__ XformParams xp,
                                                              typename DType<DT>::T* __restrict__ y, int t0) {
@@ -902,12 +980,12 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
 #pragma unroll
     for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
   const size_t qs = (size_t)K * Tp;
-  const float* src = Mw + (size_t)k * Tp + tl;
+  const MT* src = Mw + (size_t)k * Tp + tl;
 #pragma unroll
   for (int i = 0; i < D; ++i) {
     float Mi[D];
 #pragma unroll
-    for (int j = 0; j < D; ++j) Mi[j] = __ldg(src + (size_t)(i * D + j) * qs);
+    for (int j = 0; j < D; ++j) Mi[j] = ld_m(src + (size_t)(i * D + j) * qs);
     float Z[M];
 #pragma unroll
     for (int q = 0; q < M; ++q) {
@@ -938,13 +1016,78 @@ __global__ void __launch_bounds__(128) output_transform_nchw(const float* __rest
   }
 }
 
+// Tile-pair K4 for a 16-bit M (domains <= 6, one pass; reading M3): thread per
+// (tiles t, t + 1, k), so each M load of a warp is 32 x (2 tiles) = 128 B (the
+// fp32-M thread-per-tile kernel measured faster than this one on fp32 M), and
+// the transform runs on packed FFMA2, the two tiles in the two lanes of each
+// instruction: per tile the same fp32 operations in the same order as
+// output_transform_nchw (bit-identical results).
+__device__ __forceinline__ float2 ld_m2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+__device__ __forceinline__ float2 ld_m2(const __half* p) {
+  return __half22float2(__ldg(reinterpret_cast<const __half2*>(p)));
+}
+__device__ __forceinline__ float2 ld_m2(const __nv_bfloat16* p) {
+  return __bfloat1622float2(__ldg(reinterpret_cast<const __nv_bfloat162*>(p)));
+}
+template <int DT, int M, int D, typename MT>
+__global__ void __launch_bounds__(128, 8) output_transform_nchw2(const MT* __restrict__ Mw, int K, int Ho, int Wo,
+                                                              int th, int tw, int T, int Tp,
+                                                              const __grid_constant__ XformParams xp,
+                                                              typename DType<DT>::T* __restrict__ y) {
+  using Tr = DType<DT>;
+  const int t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const int k = blockIdx.y;
+  if (t >= T) return;
+  float2 Y[M][M];
+#pragma unroll
+  for (int p = 0; p < M; ++p)
+#pragma unroll
+    for (int q = 0; q < M; ++q) Y[p][q] = make_float2(0.f, 0.f);
+  const size_t qs = (size_t)K * Tp;
+  const MT* src = Mw + (size_t)k * Tp + t;   // t even, Tp a multiple of 32: aligned pairs
+#pragma unroll
+  for (int i = 0; i < D; ++i) {
+    float2 Mi[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) Mi[j] = ld_m2(src + (size_t)(i * D + j) * qs);
+    float2 Z[M];
+#pragma unroll
+    for (int q = 0; q < M; ++q) {
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < D; ++j) acc = __ffma2_rn(Mi[j], make_float2(xp.AT[q][j], xp.AT[q][j]), acc);
+      Z[q] = acc;
+    }
+#pragma unroll
+    for (int p = 0; p < M; ++p)
+#pragma unroll
+      for (int q = 0; q < M; ++q) Y[p][q] = __ffma2_rn(make_float2(xp.AT[p][i], xp.AT[p][i]), Z[q], Y[p][q]);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int tt = t + h;
+    if (tt >= T) break;
+    const int tj = tt % tw, rest = tt / tw;
+    const int ti = rest % th, n = rest / th;
+    typename Tr::T* dst = y + (((size_t)n * K + k) * Ho + (size_t)ti * M) * Wo + (size_t)tj * M;
+#pragma unroll
+    for (int p = 0; p < M; ++p) {
+      if (ti * M + p >= Ho) break;
+      float row[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) row[q] = h ? Y[p][q].y : Y[p][q].x;
+      store_tile_row<Tr, M>(dst + (size_t)p * Wo, row, Wo - tj * M);
+    }
+  }
+}
+
 // TMA-staged K4 for large domains (D >= 7): a thread per (t, k) cannot keep
 // enough of its D^2 loads in flight, so M is streamed through shared memory
 // instead.  CTA = (128-tile block, 32 output channels); one producer thread
 // loads, per channel k, the piece {128 t, 1 k, Q points} of M (Q x 512 B) into
 // a ring of NB buffers (mbarriers), four warps (thread = tile) apply
 // Y = A^T M A to it in the same fp32 order as output_transform_nchw.
-template <int DT, int M, int D>
+template <int DT, int M, int D, typename MT = float>
 __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constant__ CUtensorMap tmMl, int K, int Ho,
                                                             int Wo, int th, int tw, int T, int NB,
                                                             const __grid_constant__ XformParams xp,
@@ -956,7 +1099,7 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
   uint8_t* sm = k4t_smem_raw + ((128u - (smem_u32(k4t_smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + NB;
-  float* buf = reinterpret_cast<float*>(sm + 128);
+  MT* buf = reinterpret_cast<MT*>(sm + 128);
   const int mb = blockIdx.x, k0 = blockIdx.y * 32, nk = min(K, k0 + 32) - k0;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -970,7 +1113,7 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
       for (int j = 0; j < nk; ++j) {
         const int b = j % NB;
         if (j >= NB) mbar_wait(&empty[b], (uint32_t)(((j / NB) - 1) & 1));
-        mbar_arrive_expect_tx(&full[b], Q * 128 * 4);
+        mbar_arrive_expect_tx(&full[b], Q * 128 * (uint32_t)sizeof(MT));
         tma_load_3d(buf + (size_t)b * Q * 128, &tmMl, &full[b], mb * 128, k0 + j, 0);
       }
     }
@@ -982,7 +1125,7 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
     const int b = j % NB;
     mbar_wait(&full[b], (uint32_t)((j / NB) & 1));
     if (t < T) {
-      const float* fb = buf + (size_t)b * Q * 128 + tid;
+      const MT* fb = buf + (size_t)b * Q * 128 + tid;
       float Y[M][M];
 #pragma unroll
       for (int p = 0; p < M; ++p)
@@ -992,7 +1135,7 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
       for (int i = 0; i < D; ++i) {
         float Mi[D];
 #pragma unroll
-        for (int jj = 0; jj < D; ++jj) Mi[jj] = fb[(i * D + jj) * 128];
+        for (int jj = 0; jj < D; ++jj) Mi[jj] = sm_m(fb + (i * D + jj) * 128);
         float Z[M];
 #pragma unroll
         for (int q = 0; q < M; ++q) {
@@ -1030,8 +1173,8 @@ template <int M> struct K4N {
   static constexpr int TS = M * M * KB + 8;
 };
 
-template <int DT, int M, int D>
-__global__ void __launch_bounds__(256) output_transform_nhwc(const float* __restrict__ Mw, int K, int Ho, int Wo,
+template <int DT, int M, int D, typename MT = float>
+__global__ void __launch_bounds__(256) output_transform_nhwc(const MT* __restrict__ Mw, int K, int Ho, int Wo,
                                                              int th, int tw, int T, int Tp,
                                                              const __grid_constant__ XformParams xp,
                                                              typename DType<DT>::T* __restrict__ y) {
@@ -1053,12 +1196,12 @@ __global__ void __launch_bounds__(256) output_transform_nhwc(const float* __rest
     for (int p = 0; p < M; ++p)
 #pragma unroll
       for (int q = 0; q < M; ++q) Y[p][q] = 0.f;
-    const float* src = Mw + (size_t)k * Tp + t;
+    const MT* src = Mw + (size_t)k * Tp + t;
 #pragma unroll
     for (int i = 0; i < D; ++i) {
       float Mi[D];
 #pragma unroll
-      for (int j = 0; j < D; ++j) Mi[j] = __ldg(src + (size_t)(i * D + j) * qs);
+      for (int j = 0; j < D; ++j) Mi[j] = ld_m(src + (size_t)(i * D + j) * qs);
       float Z[M];
 #pragma unroll
       for (int q = 0; q < M; ++q) {
@@ -1116,12 +1259,13 @@ struct InArgs {
   cudaStream_t st;
 };
 struct OutArgs {
-  const float* Mw;
+  const void* Mw;   // fp32, or the 16-bit layer dtype when m16
   int K, Ho, Wo, th, tw, T, Tp, layout;
   const XformParams* xp;
   void* y;
   cudaStream_t st;
   int t0 = 0, nT = -1, disc = 0;   // chunked K4 (NCHW thread-per-tile kernel only): tiles [t0, t0 + nT)
+  int m16 = 0;                      // M stored in the layer dtype (reading M3; 16-bit layers only)
 };
 using InFn = void (*)(const InArgs&);
 using OutFn = void (*)(const OutArgs&);
@@ -1306,21 +1450,24 @@ static void launch_in(const InArgs& a) {
   if (ok) {
     gk.slot_bytes = (gk.box_bytes + 127) / 128 * 128;
     gk.SEGP = seg | 1;
-    // deepest raw ring / widest halo ring that keeps two CTAs per SM
-    const int cand[2][2] = {{3, NX + M}, {2, NX + M}};
+    // deepest raw ring / widest halo ring (groups of M rows) that keeps two CTAs per SM
+    const int cand[3][2] = {{3, 3}, {2, 4}, {2, 3}};
     size_t smem = 0;
-    for (int i = 0; i < 2; ++i) {
-      gk.NSLOT = cand[i][0], gk.RR = cand[i][1];
-      smem = 256 + (size_t)gk.NSLOT * gk.slot_bytes + (size_t)gk.RR * 32 * gk.SEGP * sizeof(PT);
-      if (smem <= 110 * 1024) break;
+    for (int i = 0; i < 3; ++i) {
+      gk.NSLOT = cand[i][0], gk.RR = cand[i][1] * M;
+      smem = 256 + 128 + (size_t)gk.NSLOT * gk.slot_bytes + (size_t)gk.RR * 32 * gk.SEGP * sizeof(PT);
+      if (smem <= 112 * 1024) break;
     }
     ok = smem <= 200 * 1024 && M <= 8;   // tiles beyond 8x8: synchronous staging (see launch_in_nhwc)
     if constexpr (M <= 8) if (ok) {
       auto kern = pick_k1_tma<DT, M, NX, D>(*a.xp);
       if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       constexpr int MAXCW = k1_maxcw(NX, D);
-      const int nthr = 32 * ((gk.TJB < MAXCW ? gk.TJB : MAXCW) + K1_CONV_WARPS);   // compute + converter warps
-      dim3 grid((a.tw + gk.TJB - 1) / gk.TJB, a.N, a.Cp / 64);
+      const int nthr = 32 * ((gk.TJB < MAXCW ? gk.TJB : MAXCW) + K1_CONV_WARPS + 1);   // compute + converter + TMA warps
+      gk.ncb = (a.tw + gk.TJB - 1) / gk.TJB;
+      gk.nItems = gk.ncb * a.N * (a.Cp / 64);
+      const int per_sm = k1_small(NX, D) && DT != WINO_F32 && smem <= 112 * 1024 ? 2 : 1;
+      const int grid = gk.nItems < per_sm * num_sms() ? gk.nItems : per_sm * num_sms();
       kern<<<grid, nthr, smem, a.st>>>(tm, gk, *a.xp, (TT*)a.V, a.qstride, a.plane);
       return;
     }
@@ -1341,44 +1488,62 @@ static void launch_in(const InArgs& a) {
   kern<<<grid, 32 * tjb, ring, a.st>>>((const TT*)a.x, a.C, a.H, a.W, a.pad, a.th, a.tw, a.Cp, tjb, vec, *a.xp,
                                        (TT*)a.V, a.qstride, a.plane);
 }
-template <int DT, int M, int D>
-static void launch_out(const OutArgs& a) {
+template <int DT, int M, int D, typename MT>
+static void launch_out_mt(const OutArgs& a) {
+  const MT* Mw = static_cast<const MT*>(a.Mw);
   using Tr = DType<DT>;
   if (a.layout == WINO_NHWC && a.nT < 0) {
     const size_t smem = (size_t)32 * K4N<M>::TS * sizeof(typename Tr::T);
     constexpr int KB = K4N<M>::KB;
-    auto kern = output_transform_nhwc<DT, M, D>;
+    auto kern = output_transform_nhwc<DT, M, D, MT>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((a.T + 31) / 32, (a.K + KB - 1) / KB);
-    kern<<<grid, 256, smem, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
+    kern<<<grid, 256, smem, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
     return;
   }
   if constexpr (D >= 7) {
     constexpr int Q = D * D;
-    int NB = a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * 4)) : 0;   // chunks: thread-per-tile kernel
+    int NB = a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * sizeof(MT))) : 0;   // chunks: thread-per-tile kernel
     NB = NB > 4 ? 4 : NB;
     CUtensorMap tml;
     const uint64_t dims[3] = {(uint64_t)a.Tp, (uint64_t)a.K, (uint64_t)Q};
-    const uint64_t str[2] = {(uint64_t)a.Tp * 4, (uint64_t)a.K * a.Tp * 4};
+    const uint64_t str[2] = {(uint64_t)a.Tp * sizeof(MT), (uint64_t)a.K * a.Tp * sizeof(MT)};
     const uint32_t box[3] = {128, 1, (uint32_t)Q};
     if (NB >= 2 && (reinterpret_cast<uintptr_t>(a.Mw) % 16) == 0 &&
-        make_map(&tml, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, a.Mw, dims, str, box, false)) {
-      const size_t smem = 256 + (size_t)NB * Q * 128 * 4;
-      auto kern = output_transform_tma<DT, M, D>;
+        make_map(&tml, sizeof(MT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : (DT == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16), 3, a.Mw, dims, str, box, false)) {
+      const size_t smem = 256 + (size_t)NB * Q * 128 * sizeof(MT);
+      auto kern = output_transform_tma<DT, M, D, MT>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       dim3 grid((a.T + 127) / 128, (a.K + 31) / 32);
       kern<<<grid, 160, smem, a.st>>>(tml, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, NB, *a.xp, (typename Tr::T*)a.y);
       return;
     }
   }
+  if (sizeof(MT) == 2 && a.nT < 0 && a.t0 == 0) {   // 16-bit M, one pass: the tile-pair kernel
+    dim3 grid((a.T + 255) / 256, a.K);
+    output_transform_nchw2<DT, M, D, MT><<<grid, 128, 0, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp,
+                                                                 (typename Tr::T*)a.y);
+    return;
+  }
   const int nT = a.nT < 0 ? a.T - a.t0 : a.nT;
   dim3 grid((nT + 127) / 128, a.K);
-  if (a.disc)
-    output_transform_nchw<DT, M, D, true><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT, a.Tp,
+  if (sizeof(MT) == 4 && a.disc)
+    output_transform_nchw<DT, M, D, true><<<grid, 128, 0, a.st>>>((const float*)a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT, a.Tp,
                                                                   *a.xp, (typename Tr::T*)a.y, a.t0);
   else
-    output_transform_nchw<DT, M, D, false><<<grid, 128, 0, a.st>>>(a.Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT,
+    output_transform_nchw<DT, M, D, false, MT><<<grid, 128, 0, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.t0 + nT,
                                                                    a.Tp, *a.xp, (typename Tr::T*)a.y, a.t0);
+}
+
+template <int DT, int M, int D>
+static void launch_out(const OutArgs& a) {
+  // 16-bit M for tiles up to 8x8 (m_in_dtype: larger tiles keep an fp32 M)
+  if constexpr (DT == WINO_F16 && M <= 8) {
+    if (a.m16) return launch_out_mt<DT, M, D, __half>(a);
+  } else if constexpr (DT == WINO_BF16 && M <= 8) {
+    if (a.m16) return launch_out_mt<DT, M, D, __nv_bfloat16>(a);
+  }
+  launch_out_mt<DT, M, D, float>(a);
 }
 
 // m in [2, 8], domain D in [m + 2, m + 4] (at most two quadratic moduli).
@@ -1386,14 +1551,9 @@ static void launch_out(const OutArgs& a) {
 // d - 1 domain points); the largest tiles (m >= 9) stop at D = m + 4.
 #define WINO_ROW(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>, &F<DT, M, M + 5>}
 #define WINO_ROW3(F, DT, M) {&F<DT, M, M + 2>, &F<DT, M, M + 3>, &F<DT, M, M + 4>, nullptr}
-#define WINO_TABLE(F, DT)                                                                                         \
-  {WINO_ROW(F, DT, 2),  WINO_ROW(F, DT, 3),  WINO_ROW(F, DT, 4),  WINO_ROW(F, DT, 5),                            \
-   WINO_ROW(F, DT, 6),  WINO_ROW(F, DT, 7),  WINO_ROW(F, DT, 8),  WINO_ROW3(F, DT, 9),                           \
-   WINO_ROW3(F, DT, 10), WINO_ROW3(F, DT, 11), WINO_ROW3(F, DT, 12)}
 constexpr int kTabM = 11, kTabD = 4;
-
-// per-dtype tables (xform_<dt>.cu)
-extern const InFn kInTableF32[kTabM][kTabD], kInTableF16[kTabM][kTabD], kInTableBF16[kTabM][kTabD];
-extern const OutFn kOutTableF32[kTabM][kTabD], kOutTableF16[kTabM][kTabD], kOutTableBF16[kTabM][kTabD];
+// the dispatch table is built in slices of m (xform.cu, one unit per dtype x kind x slice):
+// rows m = 2..5, 6..8, 9..12
+constexpr int kXfRows0 = 4, kXfRows1 = 3, kXfRows2 = 4;
 
 }  // namespace wino

@@ -1,6 +1,7 @@
 """Per-kernel CUDA-event times (K2, K1, K3, K4) and the whole step of one cfg5-shaped
 layer, for A/B comparisons of kernel variants (environment switches such as
-WINO_PAIR=0).  Random synthetic inputs (torch), no oracle.
+WINO_PAIR=0; KT_M_STORE=dtype selects M in the 16-bit dtype).  Random synthetic
+inputs (torch), no oracle.
 
     python scripts/kernel_times.py [algo] [dtype] [N] [C] [K] [H]
 """
@@ -20,6 +21,8 @@ dt = sys.argv[2] if len(sys.argv) > 2 else "bf16"
 N, C, K, H = (int(v) for v in (sys.argv[3:7] + ["256", "512", "512", "28"][len(sys.argv[3:7]):]))
 spec, m = canonical_spec(name)
 a = Wn.WinoAlgo(spec, m)
+if os.environ.get("KT_M_STORE", "fp32") == "dtype":   # M3: M stored in the 16-bit dtype
+    a.set_m_storage("dtype")
 tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[dt]
 torch.manual_seed(0)
 x = torch.relu(torch.randn(N, C, H, H, device="cuda")).to(tdt)
@@ -39,6 +42,6 @@ with torch.cuda.stream(st):
         Wn.wino_conv2d(x, w, a, out=y, workspace=ws, stream=st)
     e1.record(st)
 torch.cuda.synchronize()
-out = {"algo": name, "dtype": dt, "shape": [N, C, K, H], "env": {k: v for k, v in os.environ.items() if k.startswith("WINO_")},
+out = {"algo": name, "dtype": dt, "shape": [N, C, K, H], "env": {k: v for k, v in os.environ.items() if k.startswith(("WINO_", "KT_"))},
        "step_us_eager": e0.elapsed_time(e1) / 50 * 1e3, "kernels_us": {k: v * 1e3 for k, v in kern.items()}}
 print(json.dumps(out))

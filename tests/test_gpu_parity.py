@@ -771,3 +771,125 @@ def test_layer_scaled_transforms(name, dtype):
         torch.cuda.synchronize()
         s0 = MT.summary(MT.stats8(host(y0), yref, m))
         assert s0["mean_rel"] > 10 * sg["mean_rel"], (s0, sg)
+
+
+# --------------------------------------------------------------------------- M stored in the dtype (reading M3)
+
+
+def _m3(name, lowering="subsolver"):
+    a, ref, m = algo_pair(name, lowering)
+    a.set_m_storage("dtype")
+    return a, ref, m
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name,lowering,N,H,K", [("lin4", "subsolver", 16, 30, 512), ("lin4", "subsolver", 5, 30, 72),
+                                                 ("sup1_4", "residue", 5, 30, 136)])
+def test_domain_gemm_m_dtype_is_rounded_accumulator(dtype, name, lowering, N, H, K):
+    """K3 under WINO_M_DTYPE stores rd(M) of the same fp32 accumulation: bit for
+    bit the RNE cast of the fp32-M kernel's output (CTA-pair and one-CTA)."""
+    a32, _, m = algo_pair(name, lowering)
+    a16, _, _ = _m3(name, lowering)
+    x, w = datagen.layer(N, 136, K, H, H, dtype, seed=21)
+    U = W.wino_weight_transform(dev(w, dtype), a32)
+    V = W.wino_input_transform(dev(x, dtype), a32)
+    T_ = W.geometry(a32, N, 136, H, H, K, 1, dtype)["T"]
+    M32 = W.wino_domain_gemm(V, U, a32, 136, K, T_)
+    M16 = W.wino_domain_gemm(V, U, a16, 136, K, T_)
+    torch.cuda.synchronize()
+    assert M16.dtype == TD[dtype]
+    assert torch.equal(M16[:, :, :T_], M32[:, :, :T_].to(TD[dtype]))
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("name,layout", [("lin4", "nchw"), ("lin6", "nchw"), ("sup1_6", "nchw"), ("lin4", "nhwc")])
+def test_output_transform_m_dtype_equals_widened(dtype, name, layout):
+    """K4 reading a 16-bit M (thread-per-tile, TMA-staged for domains >= 7, NHWC)
+    computes exactly what the fp32-M K4 computes on the widened values."""
+    a32, _, m = algo_pair(name)
+    a16, _, _ = _m3(name)
+    N, K, H = 2, 72, 22
+    g = W.geometry(a32, N, 1, H, H, K, 1, dtype)
+    rng = np.random.default_rng(5)
+    M16 = torch.from_numpy(rng.standard_normal((a32.domain ** 2, K, g["Tp"]))).to(TD[dtype]).cuda()
+    y16 = W.wino_output_transform(M16, a16, N, K, H, H, 1, dtype, layout=layout)
+    y32 = W.wino_output_transform(M16.float(), a32, N, K, H, H, 1, dtype, layout=layout)
+    torch.cuda.synchronize()
+    assert torch.equal(y16, y32)
+
+
+M3_CASES = [("lin2", "subsolver", 1, 8, 8, 16, 16, 1),
+            ("lin4", "subsolver", 2, 72, 40, 19, 23, 1),
+            ("sup1_4", "subsolver", 2, 72, 40, 19, 23, 0),
+            ("lin6", "subsolver", 1, 128, 136, 30, 30, 1),
+            ("sup1_6", "subsolver", 1, 128, 136, 30, 30, 1),
+            ("lin8", "subsolver", 1, 64, 64, 26, 26, 1),
+            ("sup1_4", "residue", 2, 72, 40, 19, 23, 1),
+            ("sup1_6", "residue", 1, 128, 136, 30, 30, 1),
+            ("lin4", "subsolver", 2, 128, 320, 28, 28, 1),      # K > 256: CTA-pair K3, ragged last pair tile
+            ("sup1_10", "subsolver", 1, 64, 64, 25, 27, 1)]
+
+
+@pytest.mark.parametrize("case", M3_CASES, ids=lambda c: f"{c[0]}-{c[1]}-C{c[3]}K{c[4]}-{c[5]}x{c[6]}p{c[7]}")
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_layer_m_dtype(case, dtype):
+    """Whole layers with M in the dtype (reading M3) against the oracle's
+    m_store="dtype" pipeline: inside its elementwise forward bound, mean
+    relative error within +-10 %, the same non-finite count."""
+    name, lowering, N, C, K, H, Wd, pad = case
+    a, ref, m = _m3(name, lowering)
+    ms = "dtype" if m <= 8 else "fp32"   # tiles beyond 8x8 keep an fp32 M (include/wino.h)
+    x, w = datagen.layer(N, C, K, H, Wd, dtype, seed=4)
+    y = W.wino_conv2d(dev(x, dtype), dev(w, dtype), a, pad=pad)
+    torch.cuda.synchronize()
+    yg = host(y)
+    yref = CV.direct_conv2d_f64(x, w, pad)
+    if lowering == "subsolver":
+        yo = P.pipeline_conv2d(ref, x, w, dtype, pad, m_store=ms)
+        bound = P.elementwise_bound(ref, x, w, dtype, yref, pad, m_store=ms)
+    else:
+        yo = P.pipeline_residue_conv2d(ref, x, w, dtype, pad, m_store=ms)
+        bound = P.residue_elementwise_bound(ref, x, w, dtype, yref, pad, m_store=ms)
+    fin = np.isfinite(yo)
+    bad = (np.abs(yg - yref) > bound) & fin
+    assert not bad.any(), (int(bad.sum()), float(np.abs(yg - yref)[fin].max()))
+    sg = MT.summary(MT.stats8(yg, yref, m))
+    so = MT.summary(MT.stats8(yo, yref, m))
+    assert sg["nonfinite"] == so["nonfinite"]
+    if so["nonfinite"] == 0:
+        assert abs(sg["mean_rel"] / so["mean_rel"] - 1) <= 0.10, (sg, so)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_layer_m_dtype_nhwc_equals_nchw(dtype):
+    a, _, m = _m3("lin4")
+    x, w = datagen.layer(2, 64, 128, 28, 28, dtype, seed=8)
+    xd, wd = dev(x, dtype), dev(w, dtype)
+    y1 = W.wino_conv2d(xd, wd, a)
+    y2 = W.wino_conv2d(xd.permute(0, 2, 3, 1).contiguous(), wd, a, layout="nhwc")
+    torch.cuda.synchronize()
+    assert torch.equal(y2.permute(0, 3, 1, 2), y1)
+
+
+def test_m_dtype_is_a_no_op_for_fp32():
+    a32, _, _ = algo_pair("lin4")
+    a16, _, _ = _m3("lin4")
+    x, w = datagen.layer(1, 64, 64, 20, 20, "fp32", seed=2)
+    y1 = W.wino_conv2d(dev(x, "fp32"), dev(w, "fp32"), a32)
+    y2 = W.wino_conv2d(dev(x, "fp32"), dev(w, "fp32"), a16)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+
+
+def test_m_dtype_ranking_and_error_growth_fp16():
+    """Under M3 the superlinear F(6x6) set keeps beating the equal-ratio Toom-Cook
+    F(4x4) in fp16, on the GPU as in the oracle."""
+    errs = {}
+    for name in ("lin4", "sup1_6"):
+        a, ref, m = _m3(name)
+        x, w = datagen.layer(2, 128, 64, 28, 28, "fp16", seed=12)
+        yg = host(W.wino_conv2d(dev(x, "fp16"), dev(w, "fp16"), a))
+        yref = CV.direct_conv2d_f64(x, w, 1)
+        yo = P.pipeline_conv2d(ref, x, w, "fp16", 1, m_store="dtype")
+        errs[name] = (MT.summary(MT.stats8(yg, yref, m))["mean_rel"], MT.summary(MT.stats8(yo, yref, m))["mean_rel"])
+    assert errs["sup1_6"][0] < errs["lin4"][0] and errs["sup1_6"][1] < errs["lin4"][1], errs
