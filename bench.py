@@ -399,15 +399,16 @@ def kernel_rooflines(algo, dtype, x, w, y, ws, st, nl, C, K, H, W, reps, lay, pe
                        "TFLOP/s": (d["flops"] / (ms_ * 1e-3) / 1e12) if d["flops"] else None,
                        "bound": "tensor" if t_tc > t_mem else "hbm", "frac": max(t_mem, t_tc) / (ms_ * 1e-3)}
     dom = max(kernels, key=lambda k_: kernels[k_]["us"])
+    mkey = dtype + ("_m3" if g.get("mes", 4) == 2 else "")   # ncu summary key of this M storage
     kd = kernels[dom]
     if kd["bound"] == "tensor":
         ach = info[dom]["flops"] / (kd["us"] * 1e-6) / 1e12
         roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": tc / 1e12, "unit": "TFLOP/s",
-                "frac": ach / (tc / 1e12), "traffic": ncu_traffic(dom, a, dtype), "peak_source": peak_src}
+                "frac": ach / (tc / 1e12), "traffic": ncu_traffic(dom, a, mkey), "peak_source": peak_src}
     else:
         ach = info[dom]["bytes"] / (kd["us"] * 1e-6) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": ncu_traffic(dom, a, dtype), "peak_source": peak_src}
+                "frac": ach / peaks["hbm_gbs"], "traffic": ncu_traffic(dom, a, mkey), "peak_source": peak_src}
     if dtype == "fp32":
         roof["tf32_peak_note"] = ("3xTF32 (hi*hi + hi*lo + lo*hi); TF32 dense peak = measured bf16 %.1f TFLOP/s x 1/2 "
                                   "(nominal ratio 1.125/2.25 PFLOP/s); fp32-accurate peak = that / 3" % peaks["bf16_tflops"])
@@ -650,7 +651,7 @@ def ncu_traffic(kernel, a, dtype=None):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary, if one
     matches this workload (profiles/ncu_full_*.json), else None."""
     import glob
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json"))):
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_*.json")), reverse=True):   # newest tag first
         try:
             with open(p) as f:
                 d = json.load(f)
