@@ -383,6 +383,7 @@ struct DevState {
   bool ready = false;
   int sms = 0;
   int pair_clusters = 0;   // co-resident 2-CTA clusters of the K3 pair kernel (0: not queried yet)
+  int ures_clusters = 0;   // ... of the resident-U pair kernel
   cudaStream_t side = nullptr, io_in = nullptr, io_out = nullptr;   // K2 fork; host_io copy streams
   cudaEvent_t fork = nullptr, join = nullptr, io_ev[2][64] = {};
 };

@@ -398,6 +398,199 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
 }
 
+// ------------------------------------------------------------------ CTA pair, resident U
+// The CTA-pair GEMM with the B operand kept in shared memory.  A work unit is one
+// (point p, 256-wide k block nb) and a range of 256-tile blocks: each CTA loads its
+// 128 k rows of U_p for ALL Cp channels once (Cp <= 512: 8 swizzled 16 KB boxes,
+// 128 KB) and then streams only V through a 4-stage ring, so a CTA receives 16 KB
+// of operands per 128 x 256 x 64 step instead of 32 KB (the per-SM L2 ingress
+// that bounds the streamed-B kernel).  SUBSOLVER (identity
+// schedule), 16-bit operands.  Same accumulation order per output element as the
+// other K3 kernels (k blocks ascending, 16-element MMA steps): identical bits.
+//   barriers: as domain_gemm_pair_kernel, plus ufull (leader: 2 arrivals + both
+//   CTAs' U bytes) and uempty (each CTA, multicast commit after a unit's MMAs).
+template <int STAGES, int MT>
+struct UresCfg {
+  static constexpr int BK = 64, UK = 16, BN = 256;
+  static constexpr int A_BYTES = kBM * 128;
+  static constexpr int UBLK = 128 * 128;             // one k block of this CTA's 128 U rows
+  static constexpr int U_BYTES = 8 * UBLK;           // Cp <= 512
+  static constexpr int EPI_BYTES = 32 * kBM * 4;
+  static constexpr int SMEM = U_BYTES + STAGES * A_BYTES + 2 * EPI_BYTES + 1024 + 256;
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+
+template <int STAGES, int MT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    domain_gemm_ures_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmU,
+                            const __grid_constant__ CUtensorMap tmM, int T, int K, int Cp, int nMB2, int nNB, int Q,
+                            int nSplit, uint32_t idesc, int mb0) {
+  using Cfg = UresCfg<STAGES, MT>;
+  constexpr int BN = Cfg::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ures = smem;
+  uint8_t* astg = smem + Cfg::U_BYTES;
+  float* epi = reinterpret_cast<float*>(astg + STAGES * Cfg::A_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(epi) + 2 * Cfg::EPI_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ufull = tempty + 2;
+  uint64_t* uempty = ufull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uempty + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmU);
+    tma_prefetch(&tmM);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 2), mbar_init(&empty[s], 1);
+    for (int a = 0; a < 2; ++a) mbar_init(&tfull[a], 1), mbar_init(&tempty[a], 8);
+    mbar_init(ufull, 2), mbar_init(uempty, 1);
+    fence_barrier_init();
+    fence_proxy_async_shared();
+  }
+  if (warp == 2) tmem_alloc_pair(tmem_slot, 2 * BN);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int KB = Cp / Cfg::BK;
+  const int nWork = Q * nNB * nSplit;
+  // work w: unit (p, nb) = w / nSplit, tile-block-pair range [lo, hi) of split w % nSplit
+  auto work = [&](int w, int& p, int& nb, int& lo, int& hi) {
+    const int u = w / nSplit, sp = w % nSplit;
+    p = u / nNB, nb = u % nNB;
+    lo = (int)((long long)nMB2 * sp / nSplit), hi = (int)((long long)nMB2 * (sp + 1) / nSplit);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0, uphase = 0;
+      for (int w = cl; w < nWork; w += ncl) {
+        int p, nb, lo, hi;
+        work(w, p, nb, lo, hi);
+        if (lo >= hi) continue;
+        // this CTA's 128 U rows of (p, nb), every k block, once per unit
+        mbar_wait(uempty, uphase ^ 1);
+        const uint32_t ub = mapa_rank(ufull, 0);
+        if (rank == 0) mbar_arrive_expect_tx(ufull, 2 * KB * Cfg::UBLK);
+        else mbar_arrive_cluster(ub);
+        const int k0 = nb * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < KB; ++kb) tma_load_3d_pair(ures + kb * Cfg::UBLK, &tmU, ub, kb * Cfg::BK, k0, p);
+        uphase ^= 1;
+        for (int mb2 = lo; mb2 < hi; ++mb2) {
+          const int mb = mb0 + 2 * mb2 + (int)rank;
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t fb = mapa_rank(&full[stage], 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::A_BYTES);
+            else mbar_arrive_cluster(fb);
+            tma_load_3d_pair(astg + stage * Cfg::A_BYTES, &tmV, fb, 0, 0, (mb * KB + kb) * Q + p);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+        }
+      }
+      for (int s = 0; s < STAGES; ++s) {   // drain: every multicast arrival has landed
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (++stage == STAGES) stage = 0, phase ^= 1;
+      }
+      mbar_wait(uempty, uphase ^ 1);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0, uphase = 0;
+      for (int w = cl; w < nWork; w += ncl) {
+        int p, nb, lo, hi;
+        work(w, p, nb, lo, hi);
+        if (lo >= hi) continue;
+        mbar_wait(ufull, uphase);
+        uphase ^= 1;
+        tc_fence_after();
+        const uint32_t u0 = smem_u32(ures);
+        for (int mb2 = lo; mb2 < hi; ++mb2) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + acc * BN;
+          for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(astg + stage * Cfg::A_BYTES);
+            const uint32_t b0 = u0 + kb * Cfg::UBLK;
+#pragma unroll
+            for (int k = 0; k < Cfg::BK / Cfg::UK; ++k) {
+              const uint32_t koff = k * Cfg::UK * 2;   // 32 bytes
+              mma_ss_pair<false>(d_tmem, umma_desc_sw128(a0 + koff), umma_desc_sw128(b0 + koff), idesc,
+                                 (kb | k) != 0);
+            }
+            mma_commit_pair(&empty[stage]);
+            if (++stage == STAGES) stage = 0, phase ^= 1;
+          }
+          mma_commit_pair(&tfull[acc]);
+          if (++acc == 2) acc = 0, acc_phase ^= 1;
+        }
+        mma_commit_pair(uempty);   // the unit's MMAs (all readers of U) are done
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // -------------------------------------------------- epilogue (both CTAs)
+    const int wq = warp & 3;
+    const bool storer = (warp == 4 && lane == 0);
+    int acc = 0, chunk = 0;
+    uint32_t acc_phase = 0;
+    for (int w = cl; w < nWork; w += ncl) {
+      int p, nb, lo, hi;
+      work(w, p, nb, lo, hi);
+      for (int mb2 = lo; mb2 < hi; ++mb2) {
+        const int t0 = (2 * mb2 + (int)rank) * kBM;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(wq * 32) << 16) + acc * BN + j0, v);
+          if (j0 + 32 == BN) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_rank(&tempty[acc], 0));
+          }
+          if (nb * BN + j0 >= K || t0 >= T) continue;
+          float* buf = epi + (chunk & 1) * (Cfg::EPI_BYTES / 4);
+          if (storer) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) epi_put<MT>(buf, jj * kBM + wq * 32 + lane, v[jj]);
+          fence_proxy_async_shared();
+          named_bar_sync(1, 128);
+          if (storer) {
+            tma_store_3d(&tmM, buf, t0, nb * BN + j0, p);
+            bulk_commit();
+          }
+          ++chunk;
+        }
+        if (++acc == 2) acc = 0, acc_phase ^= 1;
+      }
+    }
+    if (storer) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, 2 * BN);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 template <bool kTF32, int STAGES, int EPI, bool kHint, int EC = 32, int MT = 0>
@@ -446,6 +639,57 @@ static wino_status launch_gemm(const CUtensorMap& tv, const CUtensorMap& tu, con
   return WINO_OK;
 }
 
+template <int STAGES, int MT>
+static wino_status launch_gemm_ures(const CUtensorMap& tv, const CUtensorMap& tu, const CUtensorMap& tm,
+                                    const Geo& g, uint32_t fmt, int mb0, int nT, cudaStream_t st) {
+  using Cfg = UresCfg<STAGES, MT>;
+  auto kern = domain_gemm_ures_kernel<STAGES, MT>;
+  WINO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  const int nMB2 = (nT + 2 * kBM - 1) / (2 * kBM), nNB = (g.K + Cfg::BN - 1) / Cfg::BN;
+  DevState* ds = dev_state();
+  if (!ds) return WINO_E_CUDA;
+  if (ds->ures_clusters == 0) {
+    cudaLaunchConfig_t qc = {};
+    qc.gridDim = dim3(2 * (ds->sms / 2), 1, 1);
+    qc.blockDim = dim3(256, 1, 1);
+    qc.dynamicSmemBytes = Cfg::SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    qc.attrs = at, qc.numAttrs = 1;
+    int ncl = 0;
+    WINO_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, kern, &qc));
+    ds->ures_clusters = ncl > 0 ? ncl : 1;
+  }
+  // units (p, nb); split each unit's tile-block range so every cluster has work
+  const int units = g.Q * nNB;
+  int nSplit = (ds->ures_clusters + units - 1) / units;
+  if (nSplit > nMB2) nSplit = nMB2;
+  if (nSplit < 1) nSplit = 1;
+  const int works = units * nSplit;
+  const int ncl = works < ds->ures_clusters ? works : ds->ures_clusters;
+  kern<<<2 * ncl, 256, Cfg::SMEM, st>>>(tv, tu, tm, nT, g.K, g.Cp, nMB2, nNB, g.Q, nSplit,
+                                        make_idesc(fmt, 2 * kBM, Cfg::BN), mb0);
+  WINO_LAUNCH_CHECK();
+  return WINO_OK;
+}
+
+// Resident-U CTA-pair K3, opt-in (WINO_URES=1): 16-bit SUBSOLVER layers with the
+// identity schedule, K > 128 and Cp <= 512.  Measured slower than the streamed-U
+// pair kernel on cfg5 lin4 (266 vs 240 us fp32 M, 217 vs 198 us 16-bit M): halving
+// the per-SM operand ingress does not pay for its shallower (4 x 16 KB) A ring and
+// the per-unit U reload bubbles.
+static bool ures_enabled() {
+  const char* e = getenv("WINO_URES");
+  return e && *e == '1';
+}
+static bool identity_sched(const GemmSched& gs) {
+  if (gs.npairs != gs.Q) return false;
+  for (int p = 0; p < gs.Q; ++p)
+    if (gs.off[p] != p || gs.in_pt[p] != p || gs.slab[p] != p) return false;
+  return true;
+}
+
 // The CTA-pair K3 is the default for 16-bit layers with K > 128 (WINO_PAIR=0 selects
 // the one-CTA kernel, for comparison).
 static bool pair_enabled() {
@@ -462,6 +706,14 @@ static wino_status launch_domain_gemm_16(const CUtensorMap& tv, const CUtensorMa
                                          const void* U, const Geo& g, const wino_algo* al, CUtensorMapDataType cdt,
                                          uint32_t fmt, int BN, int mb0, int nT, cudaStream_t st) {
   const uint32_t BK = 128 / (uint32_t)g.es;
+  if (BN == 256 && nT > kBM && pair_enabled() && ures_enabled() && g.Cp <= 512 && identity_sched(al->gs)) {
+    CUtensorMap tu2;
+    if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {
+      set_last_error("cuTensorMapEncodeTiled failed");
+      return WINO_E_CUDA;
+    }
+    return launch_gemm_ures<4, MT>(tv, tu2, tm, g, fmt, mb0, nT, st);
+  }
   if (BN == 256 && nT > kBM && pair_enabled()) {
     CUtensorMap tu2;   // B boxes of 128 k rows: each CTA of the pair loads half of the 256-wide tile
     if (!make_map3(&tu2, cdt, g.es, U, g.Cp, g.K, (uint64_t)g.S * g.planes, BK, 128)) {

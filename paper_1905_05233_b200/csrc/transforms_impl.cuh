@@ -618,12 +618,8 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS + 1), k1
           if (gr < -pad) continue;   // never read
           PT* drow = ring + (g * M + k) * 32 * SEGP;
           const TT* rrow = rs + (gr < 0 ? 0 : gr - gst) * rstride + qoff;
-          for (int b = lane; b < blo; b += 32)
-#pragma unroll 4
-            for (int p = 0; p < 32; ++p) drow[p * SEGP + b] = z;
-          for (int b = bhi + lane; b < SEG; b += 32)
-#pragma unroll 4
-            for (int p = 0; p < 32; ++p) drow[p * SEGP + b] = z;
+          for (int b = 0; b < blo; ++b) drow[lane * SEGP + b] = z;     // lane = channel pair
+          for (int b = bhi; b < SEG; ++b) drow[lane * SEGP + b] = z;
           if (gr >= 0 && allc && vec) {
             // two columns per lane and load (4-byte / 8-byte raw pairs): lanes 0-15 walk the
             // column pairs, the two half-warps take the even / odd channel pairs p
@@ -952,6 +948,9 @@ __global__ void __launch_bounds__(256, 2) input_transform_pairs(
 }
 
 // ------------------------------------------------------------------ K4 output transform (NCHW)
+#ifndef K4_TMA16
+#define K4_TMA16 1   // 16-bit M: the TMA-staged K4 at every domain size (0: tile-pair kernel for domains <= 6)
+#endif
 // M element: fp32 (reading R1) or the layer's 16-bit dtype (reading M3)
 __device__ __forceinline__ float ld_m(const float* p) { return __ldg(p); }
 __device__ __forceinline__ float ld_m(const __half* p) { return __half2float(__ldg(p)); }
@@ -1501,7 +1500,7 @@ static void launch_out_mt(const OutArgs& a) {
     kern<<<grid, 256, smem, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
     return;
   }
-  if constexpr (D >= 7) {
+  if constexpr (D >= 7 || (sizeof(MT) == 2 && K4_TMA16)) {
     constexpr int Q = D * D;
     int NB = a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * sizeof(MT))) : 0;   // chunks: thread-per-tile kernel
     NB = NB > 4 ? 4 : NB;
@@ -1519,11 +1518,13 @@ static void launch_out_mt(const OutArgs& a) {
       return;
     }
   }
-  if (sizeof(MT) == 2 && a.nT < 0 && a.t0 == 0) {   // 16-bit M, one pass: the tile-pair kernel
-    dim3 grid((a.T + 255) / 256, a.K);
-    output_transform_nchw2<DT, M, D, MT><<<grid, 128, 0, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp,
-                                                                 (typename Tr::T*)a.y);
-    return;
+  if constexpr (sizeof(MT) == 2 && D <= 8) {
+    if (a.nT < 0 && a.t0 == 0) {   // 16-bit M, one pass: the tile-pair kernel
+      dim3 grid((a.T + 255) / 256, a.K);
+      output_transform_nchw2<DT, M, D, MT><<<grid, 128, 0, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp,
+                                                                   *a.xp, (typename Tr::T*)a.y);
+      return;
+    }
   }
   const int nT = a.nT < 0 ? a.T - a.t0 : a.nT;
   dim3 grid((nT + 127) / 128, a.K);

@@ -182,6 +182,31 @@ def test_domain_gemm_pair_equals_single(dtype, T_, K, monkeypatch):
     assert torch.equal(M1[:, :, :T_], M2[:, :, :T_])
 
 
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+@pytest.mark.parametrize("T_,K,C,m_store", [(1000, 512, 200, "fp32"), (300, 384, 512, "fp32"), (1000, 512, 136, "dtype"),
+                                          (129, 260, 64, "fp32")])
+def test_domain_gemm_resident_u_equals_streamed(dtype, T_, K, C, m_store, monkeypatch):
+    """The resident-U CTA-pair K3 (opt-in WINO_URES=1: U slice kept in shared
+    memory, 16-bit SUBSOLVER layers with Cp <= 512) and the default streamed-U
+    pair kernel accumulate in the same order: identical bits, fp32 or 16-bit M."""
+    a, ref, m = algo_pair("lin4")
+    if m_store == "dtype":
+        a.set_m_storage("dtype")
+    rng = np.random.default_rng(13)
+    Q = a.domain ** 2
+    Cp = -(-C // 64) * 64
+    Vh = np.zeros((1, Q, T_, Cp))
+    Uh = np.zeros((1, Q, K, Cp))
+    Vh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, T_, C)), dtype)
+    Uh[..., :C] = datagen.to_dtype_values(rng.standard_normal((1, Q, K, C)), dtype)
+    Vd, Ud = W.v_from_dense(dev(Vh, dtype)), dev(Uh, dtype)
+    M2 = W.wino_domain_gemm(Vd, Ud, a, C, K, T_)
+    monkeypatch.setenv("WINO_URES", "1")
+    M1 = W.wino_domain_gemm(Vd, Ud, a, C, K, T_)
+    torch.cuda.synchronize()
+    assert torch.equal(M1[:, :, :T_], M2[:, :, :T_])
+
+
 def test_domain_gemm_pair_equals_single_tf32(monkeypatch):
     """fp32 (3xTF32 from hi/lo planes): the CTA-pair K3 equals the one-CTA kernel bitwise."""
     a, ref, m = algo_pair("lin4")
