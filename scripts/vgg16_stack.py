@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--sample", type=int, default=2)
     ap.add_argument("--proxy", type=int, default=32, help="images for the classifier-argmax proxy (0: off)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp16"])
+    ap.add_argument("--m-store", default="fp32", choices=["fp32", "dtype"],
+                    help="M between K3 and K4: fp32 (reading R1) or the 16-bit dtype (reading M3)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -54,15 +56,18 @@ def main():
             w = rng.normal(0.0, datagen.he_sigma(cin), (cout, cin, 3, 3))
             weights.append(torch.from_numpy(w).to(tdt).cuda())
     out = {"workload": f"BASELINE cfg4: VGG-16 conv stack, N={a.n}, 224x224x3 U[0,1), He weights, {dt}, "
-                       f"error on {a.sample} images vs fp64 direct", "peaks": peak_src,
+                       f"error on {a.sample} images vs fp64 direct", "peaks": peak_src, "m_store": a.m_store,
            "roofline_note": "per layer: frac_compulsory = max(GEMM flops / tensor peak, (x + w + y) bytes / HBM) / "
                             "time; frac_staged adds U, V and the fp32 M written and read (this design); the GEMM "
-                            "flops count the channels padded to the 64-channel block (C = 3 -> 64)", "algos": {}}
+                            "flops count the channels padded to the 64-channel block (C = 3 -> 64); M is fp32 or, with "
+                            "--m-store dtype, 16-bit", "algos": {}}
     st = torch.cuda.current_stream()
     finals = {}
     for name in a.algos.split(","):
         spec, m = canonical_spec(name)
         algo = Wn.WinoAlgo(spec, m)
+        if a.m_store == "dtype":
+            algo.set_m_storage("dtype")
         act = x0
         rows, li, total = [], 0, 0.0
         for layer in STACK:
