@@ -1,6 +1,7 @@
 // transforms_impl.cuh -- kernels of transforms.cu (see there), instantiated
-// per storage dtype by xform_f32.cu / xform_f16.cu / xform_bf16.cu.
+// per storage dtype, kind and m-range slice by xform.cu.
 #pragma once
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <type_traits>
@@ -1449,13 +1450,18 @@ static void launch_in(const InArgs& a) {
   if (ok) {
     gk.slot_bytes = (gk.box_bytes + 127) / 128 * 128;
     gk.SEGP = seg | 1;
-    // deepest raw ring / widest halo ring (groups of M rows) that keeps two CTAs per SM
-    const int cand[3][2] = {{3, 3}, {2, 4}, {2, 3}};
+    // raw slots / halo-ring groups (of M rows) that keep two CTAs per SM; the first
+    // candidate can be overridden for experiments (WINO_K1_RING="<slots>,<groups>")
+    int cand[4][2] = {{3, 3}, {3, 3}, {2, 4}, {2, 3}};
+    if (const char* e = getenv("WINO_K1_RING")) {
+      int ns = 0, rg = 0;
+      if (sscanf(e, "%d,%d", &ns, &rg) == 2 && ns >= 2 && ns <= 6 && rg >= 3 && rg <= 6) cand[0][0] = ns, cand[0][1] = rg;
+    }
     size_t smem = 0;
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < 4; ++i) {
       gk.NSLOT = cand[i][0], gk.RR = cand[i][1] * M;
       smem = 256 + 128 + (size_t)gk.NSLOT * gk.slot_bytes + (size_t)gk.RR * 32 * gk.SEGP * sizeof(PT);
-      if (smem <= 112 * 1024) break;
+      if (smem <= 112 * 1024 || (i == 0 && getenv("WINO_K1_RING"))) break;
     }
     ok = smem <= 200 * 1024 && M <= 8;   // tiles beyond 8x8: synchronous staging (see launch_in_nhwc)
     if constexpr (M <= 8) if (ok) {
@@ -1500,9 +1506,13 @@ static void launch_out_mt(const OutArgs& a) {
     kern<<<grid, 256, smem, a.st>>>(Mw, a.K, a.Ho, a.Wo, a.th, a.tw, a.T, a.Tp, *a.xp, (typename Tr::T*)a.y);
     return;
   }
-  if constexpr (D >= 7 || (sizeof(MT) == 2 && K4_TMA16)) {
+  if constexpr (D >= 7 || sizeof(MT) == 2 || M <= 8) {
     constexpr int Q = D * D;
-    int NB = a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * sizeof(MT))) : 0;   // chunks: thread-per-tile kernel
+    // fp32 M at domains <= 6 too (cfg5 lin4 bf16: 188 -> 181 us); WINO_K4_TMA32=0 selects
+    // the thread-per-tile kernel (same fp32 operation order, identical bits)
+    static const bool tma32 = [] { const char* e = getenv("WINO_K4_TMA32"); return !(e && *e == '0'); }();
+    const bool use = D >= 7 || (sizeof(MT) == 2 && K4_TMA16) || tma32;
+    int NB = use && a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * sizeof(MT))) : 0;   // chunks: thread-per-tile kernel
     NB = NB > 4 ? 4 : NB;
     CUtensorMap tml;
     const uint64_t dims[3] = {(uint64_t)a.Tp, (uint64_t)a.K, (uint64_t)Q};

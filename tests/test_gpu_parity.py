@@ -12,6 +12,7 @@ Bars (DESIGN.md "Parity bounds"):
 * 1D tiles in paper mode: bitwise equal to the oracle;
 * error statistics / fp64 direct kernels: 1e-12 relative.
 """
+import os
 import numpy as np
 import pytest
 import torch
@@ -824,6 +825,40 @@ def test_domain_gemm_m_dtype_is_rounded_accumulator(dtype, name, lowering, N, H,
     torch.cuda.synchronize()
     assert M16.dtype == TD[dtype]
     assert torch.equal(M16[:, :, :T_], M32[:, :, :T_].to(TD[dtype]))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("name,layout", [("lin4", "nchw"), ("lin3", "nchw"), ("sup1_4", "nchw")])
+def test_output_transform_tma_equals_thread_per_tile(dtype, name, layout, monkeypatch):
+    """fp32 M: the TMA-staged K4 (default) and the thread-per-tile kernel
+    (WINO_K4_TMA32=0, read once per process, so the switch runs in a subprocess)
+    apply the same fp32 operations in the same order: identical bits."""
+    import subprocess
+    import sys
+    a32, _, m = algo_pair(name)
+    N, K, H = 2, 72, 22
+    g = W.geometry(a32, N, 1, H, H, K, 1, dtype)
+    rng = np.random.default_rng(7)
+    M = rng.standard_normal((a32.domain ** 2, K, g["Tp"])).astype(np.float32)
+    y_tma = W.wino_output_transform(torch.from_numpy(M).cuda(), a32, N, K, H, H, 1, dtype, layout=layout)
+    torch.cuda.synchronize()
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "import paper_1905_05233_b200 as W\n"
+        "from paper_1905_05233_b200.algos import canonical_spec\n"
+        "s, m = canonical_spec(%r); a = W.WinoAlgo(s, m)\n"
+        "M = torch.from_numpy(np.load(sys.argv[1])).cuda()\n"
+        "y = W.wino_output_transform(M, a, %d, %d, %d, %d, 1, %r, layout=%r)\n"
+        "np.save(sys.argv[2], y.float().cpu().numpy())\n" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                                             name, N, K, H, H, dtype, layout))
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        np.save(os.path.join(td, "M.npy"), M)
+        env = dict(os.environ, WINO_K4_TMA32="0")
+        subprocess.run([sys.executable, "-c", code, os.path.join(td, "M.npy"), os.path.join(td, "y.npy")],
+                       check=True, env=env)
+        y_tpt = np.load(os.path.join(td, "y.npy"))
+    assert np.array_equal(y_tma.float().cpu().numpy(), y_tpt)
 
 
 @pytest.mark.parametrize("dtype", ["fp16", "bf16"])
