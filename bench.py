@@ -601,8 +601,9 @@ def e2e(algo, x, w, y, ws, st, nl, C, K, H, W, a, world, dist):
 
 def sweep(c, st, peaks):
     """Tile-size / polynomial-set sweep of cfg5 (BASELINE configs[4]) on one GPU,
-    m = 2..8 with linear (Toom-Cook) and one-quadratic (a^2+1) sets; each row
-    carries its own layer roofline fractions."""
+    m = 2..8 with linear (Toom-Cook) and one-quadratic (a^2+1) sets, 16-bit dtypes
+    with M in fp32 (R1) and in the dtype (M3); each row carries its own layer
+    roofline fractions."""
     import numpy as np
     import torch
     import datagen
@@ -610,7 +611,7 @@ def sweep(c, st, peaks):
     from paper_1905_05233_b200.algos import canonical_spec
     rows = []
     N, C, K, H, W = c["N"], c["C"], c["K"], c["H"], c["W"]
-    for dt in ("bf16", "fp16", "fp32"):
+    for dt, ms_ in (("bf16", "fp32"), ("bf16", "dtype"), ("fp16", "fp32"), ("fp16", "dtype"), ("fp32", "fp32")):
         tdt = {"fp32": torch.float32, "fp16": torch.float16, "bf16": torch.bfloat16}[dt]
         x64, w64 = datagen.layer(N, C, K, H, W, dt, seed=0, xdist=c["xdist"])
         x = torch.from_numpy(x64).to(tdt).cuda()
@@ -621,6 +622,8 @@ def sweep(c, st, peaks):
                      "sup1_7", "lin8", "sup1_8"):
             spec, m = canonical_spec(name)
             algo = Wn.WinoAlgo(spec, m)
+            if ms_ == "dtype":
+                algo.set_m_storage("dtype")
             y = torch.empty((N, K, H, W), dtype=tdt, device="cuda")
             ws = Wn.alloc_workspace(Wn.wino_conv2d_workspace(algo, N, C, H, W, K, 1, dt))
             for _ in range(3):
@@ -637,7 +640,8 @@ def sweep(c, st, peaks):
             g = Wn.geometry(algo, N, C, H, W, K, 1, dt)
             B = layer_bytes(N, C, K, H, W, 4 if dt == "fp32" else 2, g)
             fr = layer_fracs(ms, B, 2.0 * g["T"] * C * K * g["S"] * (3 if dt == "fp32" else 1), dt, peaks)
-            rows.append({"algo": name, "dtype": dt, "mu": algo.mu, "ratio": round(algo.ratio_2d, 4), "ms": ms,
+            rows.append({"algo": name, "dtype": dt, "m_store": ms_ if (dt != "fp32" and m <= 8) else "fp32",
+                         "mu": algo.mu, "ratio": round(algo.ratio_2d, 4), "ms": ms,
                          "tflops_direct_eq": direct_flops(N, C, K, H, W) / (ms * 1e-3) / 1e12,
                          "frac_compulsory": fr["frac_compulsory"], "frac_staged": fr["frac_staged"],
                          "rel_l1": s["rel_l1"], "mean_rel": s["mean_rel"], "nonfinite": s["nonfinite"]})
