@@ -1081,6 +1081,20 @@ __global__ void __launch_bounds__(128, 8) output_transform_nchw2(const MT* __res
   }
 }
 
+// Y through shared memory for rows stored element by element (odd m in 16-bit; 12-byte
+// rows of m = 6 measured faster with their three 4-byte stores), tiles up to 8 x 8
+#ifndef K4_STAGE_Y
+#define K4_STAGE_Y 1
+#endif
+template <int M, typename TT>
+__host__ __device__ constexpr bool k4_stage_y() {
+  return K4_STAGE_Y && M <= 8 && (M * sizeof(TT)) % 4 != 0;
+}
+template <int M, typename TT>
+constexpr size_t k4_stage_bytes() {
+  return k4_stage_y<M, TT>() ? 4 * 32 * (sizeof(TT*) + sizeof(int) + (size_t)M * M * sizeof(TT)) : 0;
+}
+
 // TMA-staged K4 for large domains (D >= 7): a thread per (t, k) cannot keep
 // enough of its D^2 loads in flight, so M is streamed through shared memory
 // instead.  CTA = (128-tile block, 32 output channels); one producer thread
@@ -1095,11 +1109,18 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
   using Tr = DType<DT>;
   using TT = typename Tr::T;
   constexpr int Q = D * D;
+  constexpr bool STG = k4_stage_y<M, TT>();
   extern __shared__ __align__(16) uint8_t k4t_smem_raw[];
   uint8_t* sm = k4t_smem_raw + ((128u - (smem_u32(k4t_smem_raw) & 127u)) & 127u);
   uint64_t* full = reinterpret_cast<uint64_t*>(sm);
   uint64_t* empty = full + NB;
   MT* buf = reinterpret_cast<MT*>(sm + 128);
+  // Y staging (STG): per compute warp 32 tile bases, their valid rows / columns, and
+  // the 32 tiles' Y as [p][tile][q] in the output dtype
+  uint8_t* stg = sm + 128 + (size_t)NB * Q * 128 * sizeof(MT);
+  TT** sbase = reinterpret_cast<TT**>(stg) + (threadIdx.x >> 5) * 32;
+  int* svalid = reinterpret_cast<int*>(stg + 4 * 32 * sizeof(TT*)) + (threadIdx.x >> 5) * 32;
+  TT* sy = reinterpret_cast<TT*>(stg + 4 * 32 * (sizeof(TT*) + sizeof(int))) + (threadIdx.x >> 5) * 32 * M * M;
   const int mb = blockIdx.x, k0 = blockIdx.y * 32, nk = min(K, k0 + 32) - k0;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -1150,13 +1171,43 @@ __global__ void __launch_bounds__(160) output_transform_tma(const __grid_constan
           for (int q = 0; q < M; ++q) Y[p][q] = fmaf(xp.AT[p][i], Z[q], Y[p][q]);
       }
       TT* dst = y + (((size_t)n * K + k0 + j) * Ho + (size_t)ti * M) * Wo + (size_t)tj * M;
+      if constexpr (STG) {
+        const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int p = 0; p < M; ++p) {
-        if (ti * M + p >= Ho) break;
-        store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
+        for (int p = 0; p < M; ++p)
+#pragma unroll
+          for (int q = 0; q < M; ++q) sy[(p * 32 + lane) * M + q] = Tr::cvt(Y[p][q]);
+        sbase[lane] = dst;
+        svalid[lane] = min(M, Ho - ti * M) | (min(M, Wo - tj * M) << 8);
+      } else {
+#pragma unroll
+        for (int p = 0; p < M; ++p) {
+          if (ti * M + p >= Ho) break;
+          store_tile_row<Tr, M>(dst + (size_t)p * Wo, Y[p], Wo - tj * M);
+        }
       }
+    } else if constexpr (STG) {
+      sbase[threadIdx.x & 31] = nullptr;
     }
     mbar_arrive(&empty[b]);
+    if constexpr (STG) {
+      // the warp's 32 tiles written row p at a time: consecutive lanes take consecutive
+      // (tile, column) elements, i.e. runs of M columns of adjacent tiles (the per-tile
+      // 2-byte stores touched a sector per lane: cfg5 lin7 bf16 K4 497 -> 275 us)
+      const int lane = threadIdx.x & 31;
+      __syncwarp();
+#pragma unroll 1
+      for (int p = 0; p < M; ++p) {
+#pragma unroll
+        for (int e0 = 0; e0 < 32 * M; e0 += 32) {
+          const int e = e0 + lane, tl = e / M, q = e - tl * M;
+          TT* bp = sbase[tl];
+          const int v = svalid[tl];
+          if (bp != nullptr && p < (v & 255) && q < (v >> 8)) bp[(size_t)p * Wo + q] = sy[p * 32 * M + e];
+        }
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -1512,15 +1563,20 @@ static void launch_out_mt(const OutArgs& a) {
     // the thread-per-tile kernel (same fp32 operation order, identical bits)
     static const bool tma32 = [] { const char* e = getenv("WINO_K4_TMA32"); return !(e && *e == '0'); }();
     const bool use = D >= 7 || (sizeof(MT) == 2 && K4_TMA16) || tma32;
-    int NB = use && a.nT < 0 ? (int)((96 * 1024) / ((size_t)Q * 128 * sizeof(MT))) : 0;   // chunks: thread-per-tile kernel
+    // ring of NB buffers in <= 96 KB; domains whose Q x 128 piece exceeds 48 KB (D >= 10
+    // in fp32) take two buffers (up to 200 KB) rather than the thread-per-tile kernel
+    // (cfg5 bf16 sup1_7 K4 692 -> 441 us, lin8 331 -> 288 us); chunks: thread-per-tile kernel
+    const size_t piece = (size_t)Q * 128 * sizeof(MT);
+    int NB = use && a.nT < 0 ? (int)((96 * 1024) / piece) : 0;
     NB = NB > 4 ? 4 : NB;
+    if (use && a.nT < 0 && NB < 2 && 256 + 2 * piece + k4_stage_bytes<M, typename Tr::T>() <= 200 * 1024) NB = 2;
     CUtensorMap tml;
     const uint64_t dims[3] = {(uint64_t)a.Tp, (uint64_t)a.K, (uint64_t)Q};
     const uint64_t str[2] = {(uint64_t)a.Tp * sizeof(MT), (uint64_t)a.K * a.Tp * sizeof(MT)};
     const uint32_t box[3] = {128, 1, (uint32_t)Q};
     if (NB >= 2 && (reinterpret_cast<uintptr_t>(a.Mw) % 16) == 0 &&
         make_map(&tml, sizeof(MT) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : (DT == WINO_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16), 3, a.Mw, dims, str, box, false)) {
-      const size_t smem = 256 + (size_t)NB * Q * 128 * sizeof(MT);
+      const size_t smem = 256 + (size_t)NB * Q * 128 * sizeof(MT) + k4_stage_bytes<M, typename Tr::T>();
       auto kern = output_transform_tma<DT, M, D, MT>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       dim3 grid((a.T + 127) / 128, (a.K + 31) / 32);

@@ -245,8 +245,11 @@ def test_domain_gemm_tf32x3():
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "fp16", "bf16"])
-@pytest.mark.parametrize("name,lowering", [("lin4", "subsolver"), ("sup1_6", "subsolver"), ("sup1_4", "residue")])
+@pytest.mark.parametrize("name,lowering", [("lin4", "subsolver"), ("sup1_6", "subsolver"), ("sup1_4", "residue"),
+                                           ("lin5", "subsolver"), ("sup1_7", "subsolver"), ("lin8", "subsolver")])
 def test_output_transform(dtype, name, lowering):
+    """K4 alone vs the oracle's separable A^T M A on a ragged 17 x 13 output (odd m in
+    16-bit: Y staged through shared memory; D = 10: the two-buffer TMA ring)."""
     a, ref, m = algo_pair(name, lowering)
     N, K, H, Wd = 2, 20, 17, 13
     Ho, Wo, th, tw = CV.tile_grid(H, Wd, m, 1)
