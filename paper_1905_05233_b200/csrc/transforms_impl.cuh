@@ -375,6 +375,9 @@ __device__ __forceinline__ void transform_tile_pairs(const float2* ring, int s0,
 // with the previous tile row are reused, so x is read from HBM once.
 //   mode 0 (flat): rows are whole image rows, box {RB * W, 64} of the
 //                  [N*C][H*W] view (any W with H*W*es % 16 == 0)
+//   mode 2 (flat, row groups): the same rows as box {ralign * W, RB / ralign, 64} of the
+//                  [N*C][H / ralign][ralign * W] view -- the identical shared-memory image
+//                  for RB * W > 256, the box-dimension limit (m = 8 at W = 28 in 16 bits)
 //   mode 1 (3D):   box {BOXC, RB, 64} of the [N*C][H][W] view (W*es % 16 == 0)
 // TMA zero-fills rows / columns outside the image.
 template <int DT> struct PairT;
@@ -478,8 +481,15 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
         asm volatile("" ::: "memory");
       }
     } else {
+      // tiles from 9 x 9: a clobber keeps the halo loads inside the pass -- hoisted out of
+      // the loop they hold NX^2 registers and the kernel spills (cfg5 bf16 K1: lin8 418 ->
+      // 290 us, sup1_8 513 -> 341 us, lin7 260 -> 249 us); 8 x 8 halos are faster hoisted
+      // (sup1_6 335 vs 362 us)
 #pragma unroll 1
-      for (int j0 = 0; j0 < D; j0 += JC) pass(j0);
+      for (int j0 = 0; j0 < D; j0 += JC) {
+        pass(j0);
+        if constexpr (NX >= 9) asm volatile("" ::: "memory");
+      }
     }
   }
 }
@@ -491,6 +501,10 @@ constexpr int K1_CONV_WARPS = K1_CONV_WARPS_DEF;   // converter warps of input_t
 // compute warps per CTA: 7 for the fully unrolled small tiles, 5 for the rolled
 // larger ones (keeps two CTAs per SM with room for their registers)
 __host__ __device__ constexpr bool k1_small(int NX, int D) { return NX * D <= 36; }
+// Eight compute warps for the rolled multi-pass tiles, two warps sharing a tile's passes
+// (a tile row of cfg5 holds only 4-5 such tiles), measured no faster once the halo loads stay
+// inside the passes, and slower through the 157-register cap and the runtime pass stride
+// (cfg5 bf16 K1: lin8 301 vs 294 us, sup1_6 380-388 vs 335 us, lin5 304 vs 226 us): not kept.
 __host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_small(NX, D) ? 7 : 5; }
 
 struct K1Geo {
@@ -574,9 +588,10 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS + 1), k1
         for (int it = -1; it < th; ++it) {
           mbar_wait_sleep(&raw_empty[s], ph ^ 1);
           const int g0 = it * M - pad + NX - M;
-          const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
+          const int gst = gk.mode != 1 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
           mbar_arrive_expect_tx(&raw_full[s], gk.box_bytes);
           if (gk.mode == 0) tma_load_2d(raw + (size_t)s * gk.slot_bytes, &tmx, &raw_full[s], gst * W, crow);
+          else if (gk.mode == 2) tma_load_3d(raw + (size_t)s * gk.slot_bytes, &tmx, &raw_full[s], 0, gst / gk.ralign, crow);
           else tma_load_3d(raw + (size_t)s * gk.slot_bytes, &tmx, &raw_full[s], cst, gst, crow);
           if (++s == NSLOT) s = 0, ph ^= 1;
         }
@@ -593,12 +608,13 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS + 1), k1
       decode(item, cb, n, c0);
       const int col0 = cb * gk.TJB * M - pad;
       const int cst = ((col0 < 0 ? 0 : col0) / gk.calign) * gk.calign;
-      const int RBW = gk.mode == 0 ? gk.RB * W : gk.RB * gk.BOXC;   // elements per channel in the box
-      const int rstride = gk.mode == 0 ? W : gk.BOXC;
+      const bool flat = gk.mode != 1;                               // whole image rows (modes 0 and 2)
+      const int RBW = flat ? gk.RB * W : gk.RB * gk.BOXC;           // elements per channel in the box
+      const int rstride = flat ? W : gk.BOXC;
       // ring columns [blo, bhi) are inside the image; the others are zero
       const int blo = col0 < 0 ? -col0 : 0;
-      const int bhi = gk.mode == 0 ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
-      const int qoff = gk.mode == 0 ? col0 : col0 - cst;   // raw column of ring column b: b + qoff
+      const int bhi = flat ? (W - col0 < SEG ? W - col0 : SEG) : SEG;
+      const int qoff = flat ? col0 : col0 - cst;   // raw column of ring column b: b + qoff
       const bool allc = c0 + 64 <= gk.C;                   // every channel of the block is real
       // vector conversion: raw columns qoff + b for b in [bs, bs + 2 npair) in aligned pairs
       // (rows and channel planes of the box start at even elements), single leading /
@@ -612,7 +628,7 @@ __global__ void __launch_bounds__(32 * (k1_maxcw(NX, D) + K1_CONV_WARPS + 1), k1
         mbar_wait_sleep(&grp_empty[g], phg ^ 1);
         const TT* rs = reinterpret_cast<const TT*>(raw + (size_t)s * gk.slot_bytes);
         const int g0 = it * M - pad + NX - M;
-        const int gst = gk.mode == 0 ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
+        const int gst = flat ? ((g0 < 0 ? 0 : g0) / gk.ralign) * gk.ralign : (g0 < 0 ? 0 : g0);
 #pragma unroll 1
         for (int k = cwarp; k < M; k += K1_CONV_WARPS) {
           const int gr = g0 + k;
@@ -1486,14 +1502,23 @@ static void launch_in(const InArgs& a) {
     while ((r16 * a.W * es) % 16) ++r16;      // rows per 16-byte aligned flat offset
     gk.ralign = r16, gk.calign = 1;
     gk.RB = (M + r16 - 1 + r16 - 1) / r16 * r16;  // covers M rows from an aligned start
-    ok = gk.RB * a.W <= 256;
-    if (ok) {
+    if (gk.RB * a.W <= 256) {
       const uint64_t dims[2] = {(uint64_t)a.H * a.W, (uint64_t)a.N * a.C};
       const uint64_t str[1] = {(uint64_t)a.H * a.W * es};
       const uint32_t box[2] = {(uint32_t)(gk.RB * a.W), 64};
       ok = make_map(&tm, cdt, 2, a.x, dims, str, box, false);
-      gk.box_bytes = (unsigned)(gk.RB * a.W * 64 * es);
+    } else if (r16 * a.W <= 256 && a.H % r16 == 0) {
+      // more than 256 elements per channel: the rows as groups of r16 (16-byte aligned
+      // groups; H * W * es % 16 == 0 makes H a multiple of r16), same bytes in shared memory
+      gk.mode = 2;
+      const uint64_t dims[3] = {(uint64_t)r16 * a.W, (uint64_t)(a.H / r16), (uint64_t)a.N * a.C};
+      const uint64_t str[2] = {(uint64_t)r16 * a.W * es, (uint64_t)a.H * a.W * es};
+      const uint32_t box[3] = {(uint32_t)(r16 * a.W), (uint32_t)(gk.RB / r16), 64};
+      ok = make_map(&tm, cdt, 3, a.x, dims, str, box, false);
+    } else {
+      ok = false;
     }
+    gk.box_bytes = (unsigned)(gk.RB * a.W * 64 * es);
   } else {
     ok = false;
   }

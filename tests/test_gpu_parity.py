@@ -88,12 +88,15 @@ def test_weight_transform(dtype, name, lowering):
 @pytest.mark.parametrize("name,lowering,pad", [("lin4", "subsolver", 1), ("sup1_6", "subsolver", 1),
                                                ("lin3", "subsolver", 0), ("sup1_4", "residue", 1),
                                                ("lin8", "subsolver", 1)])
-@pytest.mark.parametrize("shape", [(2, 40, 19, 23), (2, 40, 28, 28), (1, 72, 18, 32), (2, 8, 14, 14)],
-                         ids=["odd-sync", "w28-flat16-3d32", "w32-3d", "w14-flat"])
+@pytest.mark.parametrize("shape", [(2, 40, 19, 23), (2, 40, 28, 28), (1, 72, 18, 32), (2, 8, 14, 14),
+                                   (3, 128, 28, 28)],
+                         ids=["odd-sync", "w28-flat16-3d32", "w32-3d", "w14-flat", "w28-c128"])
 def test_input_transform(dtype, name, lowering, pad, shape):
     """K1 vs the oracle's pipeline-mode V (rd(B^T d B), Eq. 2) on shapes that
     reach each staging path: odd planes (synchronous), W*es % 16 != 0 with whole
-    rows (TMA flat boxes), W*es % 16 == 0 (TMA 3D boxes), channels < 64."""
+    rows (TMA flat boxes; row-group boxes when a step's rows exceed 256 elements,
+    lin8 at W = 28 in 16 bits), W*es % 16 == 0 (TMA 3D boxes), channels < 64, and
+    full 64-channel blocks over several persistent work items (vector converter)."""
     a, ref, m = algo_pair(name, lowering)
     N, C, H, Wd = shape
     x, _ = datagen.layer(N, C, 1, H, Wd, dtype, seed=4)
