@@ -500,13 +500,14 @@ __device__ __forceinline__ void transform_tile_ring(const PT* ring, int s0, int 
 constexpr int K1_CONV_WARPS = K1_CONV_WARPS_DEF;   // converter warps of input_transform_tma
 // compute warps per CTA: 7 for the fully unrolled small tiles, 5 for the rolled
 // larger ones (keeps two CTAs per SM with room for their registers), 6 for 7 x 7 halo
-// tiles (m = 5: a tile row of 28 columns holds 6 tiles; cfg5 bf16 lin5 K1 226 -> 195 us)
+// tiles (m = 5: a tile row of 28 columns holds 6 tiles; cfg5 bf16 K1 lin5 226 -> 195 us,
+// sup1_5 234 -> 202 us)
 __host__ __device__ constexpr bool k1_small(int NX, int D) { return NX * D <= 36; }
 // Eight compute warps for the rolled multi-pass tiles, two warps sharing a tile's passes
 // (a tile row of cfg5 holds only 4-5 such tiles), measured no faster once the halo loads stay
 // inside the passes, and slower through the 157-register cap and the runtime pass stride
 // (cfg5 bf16 K1: lin8 301 vs 294 us, sup1_6 380-388 vs 335 us, lin5 304 vs 226 us): not kept.
-__host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_small(NX, D) ? 7 : NX * D <= 49 ? 6 : 5; }
+__host__ __device__ constexpr int k1_maxcw(int NX, int D) { return k1_small(NX, D) ? 7 : NX * D <= 56 ? 6 : 5; }
 
 struct K1Geo {
   int C, H, W, pad, th, tw, Cp, TJB;
